@@ -1,0 +1,430 @@
+"""Benchmark of the B200 quantized-linear hot path (BASELINE.json configs[1]).
+
+Workload ("step"): one W8A8 quantized linear at the PixArt-alpha 1024px fc1
+shape, M=4096 tokens x K=1152 -> N=4608, with static-dynamic channel
+balancing (smooth scales + 128-blockwise Hadamard) fused into the per-token
+activation quantizer, fp16 in / fp16 out:
+    fused quantizer (fq_kernel)  ->  tcgen05 i8 GEMM + dequant epilogue (qgemm_kernel)
+Inputs are resident in HBM; L2 (126 MB) is flushed with a 512 MB write
+before every timed step (the working set, ~57 MB, would otherwise fit).
+
+`value`  = whole-job INT8 TOPS (2*M*N*K per rank per step / max-over-ranks time)
+`e2e`    = the same through dtq_qlinear_forward_host (pinned host fp16 in,
+           host fp16 out, H2D + D2H inside the timed region)
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/libdtq_ref.so, compiled from the reference sources) on the
+host cores: apply_scaling + rotate_channels (per 128 block) +
+qlinear_forward, row-sliced over all threads, on a bounded row sample.
+
+Multi-GPU (torchrun): token rows shard with weights replicated, no
+collective in the timed region; each rank runs the full per-rank workload
+(weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M, K, N = 4096, 1152, 4608
+WBITS, ABITS, HBLOCK = 8, 8, 128
+METRIC = "quant-linear INT8 TOPS + STDiT block-linear latency vs FP16 cuBLAS, 1/2/4/8 GPU"
+WORKLOAD = ("W8A8 quantized linear, PixArt-alpha 1024px fc1 (M=4096, K=1152, N=4608), "
+            "smooth + 128-block Hadamard fused into the per-token quantizer, fp16 in/out")
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+def make_inputs(seed: int = 1234):
+    """SURVEY.md section 8d recipe: N(0,1) x log-normal channel gains, 4 outlier
+    channels x30; W ~ N(0, 1/sqrt(K)); smooth from a separate calibration draw
+    (alpha 0.5); signs from std::mt19937_64(7)."""
+    rng = np.random.default_rng(seed)
+    g = np.exp(rng.standard_normal(K))
+    out_ch = rng.choice(K, 4, replace=False)
+    x = rng.standard_normal((M, K)) * g
+    x[:, out_ch] *= 30
+    x = x.astype(np.float16)
+    w = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float16)
+    xcal = rng.standard_normal((512, K)) * g
+    xcal[:, out_ch] *= 30
+    a = np.abs(xcal).max(0)
+    b = np.abs(w.astype(np.float64)).max(0)
+    smooth = np.where((a > 0) & (b > 0), np.clip(a ** 0.5 / b ** 0.5, 1e-5, 1e5), 1.0)
+    return x, w, smooth
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [t.strip() for t in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------- CPU arms
+def cpu_reference_sample(rows: int, threads: int, x, w, smooth, signs):
+    """One bounded sample of the workload through the reference library:
+    apply_scaling + rotate_channels (128 blocks) + make_quant_linear weights
+    (prepared once, outside) + qlinear_forward on `rows` token rows."""
+    from oracle.oracle import Reference
+    ref = Reference()
+    xs = x[:rows].astype(np.float64)
+    wd = w.astype(np.float64)
+    t0 = time.perf_counter()
+    xb, wb = ref.apply_scaling(xs, wd, smooth)
+    xb = ref.rotate_blocks(xb, signs, HBLOCK)
+    t_bal = time.perf_counter() - t0
+    wc, sw, zw = _ref_weights_cache(ref, wb, smooth)
+    t1 = time.perf_counter()
+    ref.qlinear_forward(xb, wc, sw, zw, WBITS, None, ABITS, threads=threads)
+    t_lin = time.perf_counter() - t1
+    return t_bal + t_lin
+
+
+_WCACHE = {}
+
+
+def _ref_weights_cache(ref, wb, smooth):
+    key = id(smooth)
+    if key not in _WCACHE:
+        from oracle.oracle import Reference  # noqa: F401
+        signs = _SIGNS
+        wr = ref.rotate_blocks(wb, signs, HBLOCK)
+        _WCACHE[key] = ref.make_quant_linear(wr, WBITS, ABITS)
+    return _WCACHE[key]
+
+
+_SIGNS = None
+
+
+def run_reference(args, world, rank):
+    global _SIGNS
+    if rank != 0:
+        return
+    import paper_2406_02540_b200 as dtq
+    threads = os.cpu_count() or 1
+    x, w, smooth = make_inputs()
+    _SIGNS = dtq.hadamard_signs(K, 7)
+    rows = args.cpu_rows
+    for _ in range(args.warmup):
+        cpu_reference_sample(min(rows, 64), threads, x, w, smooth, _SIGNS)
+    times = [cpu_reference_sample(rows, threads, x, w, smooth, _SIGNS) for _ in range(args.steps)]
+    t = float(np.mean(times))
+    ops = 2.0 * rows * N * K
+    tops = ops / t / 1e12
+    out = {
+        "metric": METRIC, "impl": "reference", "value": tops, "unit": "TOPS",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3 * (M / rows), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "global_batch": M * args.gpus, "seq_len": M,
+                   "parallelism": f"dp{args.gpus}"},
+        "cpu_baseline": {"value": tops, "unit": "TOPS", "cores": threads, "kind": "reference",
+                         "sample": f"{rows} of {M} token rows per step (row-local, exact), "
+                                   "apply_scaling + rotate_channels + qlinear_forward"},
+        "e2e": {"value": tops, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------- GPU arm
+def run_ours(args, world, rank, local):
+    import torch
+    import paper_2406_02540_b200 as dtq
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    x_np, w_np, smooth_np = make_inputs(seed=1234)
+    signs = dtq.hadamard_signs(K, 7)
+    x = torch.from_numpy(x_np).to(dev)
+    w = torch.from_numpy(w_np).to(dev)
+    bal = dtq.Balance(torch.from_numpy(smooth_np).to(dev), torch.from_numpy(signs).to(dev), HBLOCK)
+    layer = dtq.QuantLinear.create(w, WBITS, ABITS, balance=bal)
+    y = torch.empty((M, N), dtype=torch.float16, device=dev)
+    ws = layer.workspace(M, dev)
+    ldc = (K + 15) // 16 * 16
+    codes = ws[: M * ldc].view(M, ldc)[:, :K]
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    # the two launches of one step, separately event-timed
+    from paper_2406_02540_b200 import _stream  # noqa: F401
+
+    def quantize():
+        # same call the fused forward makes, split so each kernel is timed
+        b = bal._c()
+        dtq._check(dtq.lib().dtq_quantize_rows(
+            x.data_ptr(), dtq.F16, M, K, K, ABITS, 0, dtq.MODE_FAST, dtq._ref_or_none(b), None,
+            ws.data_ptr(), ldc, s_x.data_ptr(), z_x.data_ptr(), None, stream.cuda_stream))
+
+    s_x = torch.empty(M, dtype=torch.float64, device=dev)
+    z_x = torch.empty(M, dtype=torch.int32, device=dev)
+
+    def gemm():
+        layer.gemm(codes, s_x, z_x, out=y)
+
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        quantize()
+        gemm()
+        layer.forward(x, out=y, workspace=ws)
+    torch.cuda.synchronize()
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)          # L2 flush outside the timed events
+            ev[i][0].record(stream)
+            quantize()
+            ev[i][1].record(stream)
+            gemm()
+            ev[i][2].record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    t_fq = float(np.mean([a.elapsed_time(b) for a, b, _ in ev])) * 1e-3
+    t_gm = float(np.mean([b.elapsed_time(c) for _, b, c in ev])) * 1e-3
+    t_step = max_over_ranks(t_fq + t_gm, world)
+    ops = 2.0 * M * N * K
+    value = ops * world / t_step / 1e12
+
+    # fused single-call forward (what a user calls), same flush discipline
+    fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        fev[i][0].record(stream)
+        layer.forward(x, out=y, workspace=ws)
+        fev[i][1].record(stream)
+    torch.cuda.synchronize()
+    t_fwd = float(np.mean([a.elapsed_time(b) for a, b in fev])) * 1e-3
+
+    # e2e: host fp16 in, host fp16 out through the C-ABI host entry point
+    xh = torch.from_numpy(x_np).pin_memory()
+    yh = torch.empty((M, N), dtype=torch.float16).pin_memory()
+    for _ in range(max(1, args.warmup)):
+        layer.forward_host(xh, yh)
+    barrier(world)
+    eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for i in range(args.steps):
+        eev[i][0].record(stream)
+        layer.forward_host(xh, yh)
+        eev[i][1].record(stream)
+    torch.cuda.synchronize()
+    t_e2e = max_over_ranks(float(np.mean([a.elapsed_time(b) for a, b in eev])) * 1e-3, world)
+
+    # FP16 cuBLAS comparator on the same shape (library call, reported only)
+    xw = x.clone()
+    for _ in range(3):
+        torch.matmul(xw, w.t())
+    hev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        hev[i][0].record(stream)
+        torch.matmul(xw, w.t(), out=y)
+        hev[i][1].record(stream)
+    torch.cuda.synchronize()
+    t_f16 = float(np.mean([a.elapsed_time(b) for a, b in hev])) * 1e-3
+
+    # cuBLASLt int8 (torch._int_mm) on the same shape: library INT8 reference point
+    t_i8 = None
+    try:
+        a8 = torch.randint(-127, 127, (M, K), dtype=torch.int8, device=dev)
+        b8 = torch.randint(-127, 127, (K, N), dtype=torch.int8, device=dev).t().contiguous().t()
+        for _ in range(3):
+            torch._int_mm(a8, b8)
+        iev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            iev[i][0].record(stream)
+            torch._int_mm(a8, b8)
+            iev[i][1].record(stream)
+        torch.cuda.synchronize()
+        t_i8 = float(np.mean([a.elapsed_time(b) for a, b in iev])) * 1e-3
+    except Exception:
+        t_i8 = None
+
+    if rank != 0:
+        return
+    hbm, bf16, peak_src = load_peaks()
+    int8_peak = 2.0 * bf16   # dense int8 = 2x dense bf16 on B200 (4.5 vs 2.25 PF nominal)
+    gemm_tops = ops / t_gm / 1e12
+    fq_bytes = 2 * M * K + M * K + 12 * M
+    fq_gbs = fq_bytes / t_fq / 1e9
+    gemm_bytes = M * K + N * K * WBITS // 8 + 2 * M * N + 12 * M + 12 * N
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        global _SIGNS
+        _SIGNS = signs
+        threads = os.cpu_count() or 1
+        rows = args.cpu_rows
+        tc = cpu_reference_sample(rows, threads, x_np, w_np, smooth_np, signs)
+        cpu = {"value": 2.0 * rows * N * K / tc / 1e12, "unit": "TOPS", "cores": threads,
+               "kind": "reference",
+               "sample": f"{rows} of {M} token rows (row-local, exact): reference apply_scaling "
+                         "+ rotate_channels per 128 block + qlinear_forward, row-sliced threads"}
+    prof = os.path.join(ROOT, "profiles", "latest_traffic.json")
+    traffic = None
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("qgemm_kernel_dram_bytes")
+        except Exception:
+            traffic = None
+    out = {
+        "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8xs8->s32 (fp16 in/out)",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "M_per_rank": M, "K": K, "N": N,
+                   "global_batch": M * world, "seq_len": M, "parallelism": f"dp{world}",
+                   "weights": "W8 per-out-channel symmetric, random init",
+                   "l2": "flushed (512 MB write) before every timed step"},
+        "roofline": {"bound": "tensor", "achieved": gemm_tops, "peak": int8_peak,
+                     "unit": "TFLOP/s", "frac": gemm_tops / int8_peak, "traffic": traffic,
+                     "kernel": "qgemm_kernel (tcgen05.mma kind::i8)",
+                     "peak_source": f"2 x {peak_src} dense bf16 ({bf16:.1f} TF/s); "
+                                    "nominal int8 dense 4500 TOPS",
+                     "frac_of_nominal": gemm_tops / 4500.0,
+                     "algorithmic_bytes": gemm_bytes},
+        "fused_quantizer": {"bound": "hbm", "achieved": fq_gbs, "peak": hbm, "unit": "GB/s",
+                            "frac": fq_gbs / hbm, "ms": t_fq * 1e3, "bytes": fq_bytes,
+                            "peak_source": peak_src},
+        "kernel_ms": {"fused_quantizer": t_fq * 1e3, "qgemm": t_gm * 1e3,
+                      "fused_forward_call": t_fwd * 1e3},
+        "fp16_cublas": {"ms": t_f16 * 1e3, "tflops": ops / t_f16 / 1e12,
+                        "speedup_of_ours": t_f16 / t_step},
+        "int8_cublaslt": None if t_i8 is None else {"ms": t_i8 * 1e3, "tops": ops / t_i8 / 1e12,
+                                                    "note": "torch._int_mm s8xs8, no epilogue"},
+        "e2e": {"value": ops * world / t_e2e / 1e12, "unit": "TOPS",
+                "h2d_bytes_per_step": 2 * M * K, "d2h_bytes_per_step": 2 * M * N,
+                "ms": t_e2e * 1e3, "api": "dtq_qlinear_forward_host"},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-rows", type=int, default=512)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    world, rank, local = dist_setup()
+    run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,187 @@
+/*
+ * dtq_capi.h -- C ABI of the B200 (sm_100a) quantized-linear path.
+ *
+ * This is the drop-in boundary for the reference's L1 numerics core
+ * (/root/reference/proj/core/include/dtq/{quant,balance,qgemm,plan}.hpp).
+ * Plain pointers, sizes and status codes only: no C++ or torch types.
+ * Every device-side entry point is stream-ordered on the given CUDA stream
+ * (`stream` is a cudaStream_t passed as void*; NULL = legacy default) and
+ * never synchronises unless documented.  Device pointers are marked [dev],
+ * host pointers [host].
+ *
+ * Status codes mirror the reference's exception types:
+ *   DTQ_OK                    success
+ *   DTQ_ERR_INVALID_ARGUMENT  std::invalid_argument (shape/bits/non-finite)
+ *   DTQ_ERR_OVERFLOW          std::overflow_error (accumulator bound)
+ *   DTQ_ERR_CUDA              CUDA runtime/driver failure
+ *   DTQ_ERR_UNSUPPORTED       std::logic_error (not available on this build)
+ * dtq_last_error() returns the calling thread's last message.
+ *
+ * There is no CPU fallback: without a sm_100 device every compute entry
+ * point fails with DTQ_ERR_CUDA.
+ */
+#ifndef DTQ_CAPI_H
+#define DTQ_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DTQ_CAPI_VERSION 1
+
+typedef enum dtq_status {
+  DTQ_OK = 0,
+  DTQ_ERR_INVALID_ARGUMENT = 1,
+  DTQ_ERR_OVERFLOW = 2,
+  DTQ_ERR_CUDA = 3,
+  DTQ_ERR_UNSUPPORTED = 4
+} dtq_status;
+
+/* element types of activations / outputs */
+typedef enum dtq_dtype {
+  DTQ_F16 = 0,
+  DTQ_BF16 = 1,
+  DTQ_F32 = 2,
+  DTQ_F64 = 3,
+  DTQ_S32 = 4 /* output only: zero-point-corrected integer accumulator */
+} dtq_dtype;
+
+/* arithmetic of the activation quantizer */
+typedef enum dtq_mode {
+  /* fp32 transforms; codes/s/z bit-identical to the reference when no
+   * prologue, smoothing or rotation is applied (tie-guarded fp64 divide) */
+  DTQ_MODE_FAST = 0,
+  /* fp64 transforms in the reference's operation order: bit-identical to
+   * the reference with smoothing and rotation as well */
+  DTQ_MODE_EXACT = 1
+} dtq_mode;
+
+/* prologue fused in front of the quantizer (one HBM pass) */
+typedef enum dtq_prologue_kind {
+  DTQ_PROLOGUE_NONE = 0,
+  DTQ_PROLOGUE_MODULATE = 1,    /* x*(1+scale[c])+shift[c]   toydit.cpp:339-369 */
+  DTQ_PROLOGUE_GELU = 2,        /* 0.5x(1+erf(x/sqrt2))      toydit.cpp:83      */
+  DTQ_PROLOGUE_LN_MODULATE = 3  /* LayerNorm (no affine, eps) then modulate;
+                                   no reference oracle: parity unpinned      */
+} dtq_prologue_kind;
+
+typedef struct dtq_prologue {
+  int32_t kind;        /* dtq_prologue_kind */
+  const float* scale;  /* [dev] [K] (MODULATE / LN_MODULATE) */
+  const float* shift;  /* [dev] [K] */
+  float eps;           /* LN_MODULATE */
+} dtq_prologue;
+
+/* BalanceTransform (balance.hpp:31-34): mask then rotation, both optional.
+ * The rotation is blockwise: I_{K/hblock} (x) (D * H_hblock / sqrt(hblock)),
+ * which is the reference rotate_channels when hblock == K. */
+typedef struct dtq_balance {
+  const double* smooth; /* [dev] [K] ScalingMask.s (X / s, W * s) or NULL     */
+  const int8_t* signs;  /* [dev] [K] RotationMatrix.sign_diag (+-1) or NULL   */
+  int32_t hblock;       /* rotation block, power of two in [8, 256]           */
+} dtq_balance;
+
+/* opaque quantized-linear handle (QuantLinear, qgemm.hpp:17-24) */
+typedef struct dtq_qlinear_s* dtq_qlinear_t;
+
+/* ---------------------------------------------------------------- misc */
+const char* dtq_last_error(void);
+int dtq_capi_version(void);
+/* 0 if a usable sm_100 device is current, else DTQ_ERR_CUDA */
+int dtq_device_check(void);
+
+/* ---------------------------------------------------------------- quantizer
+ * quantize(x, per_token | per_output_channel, bits, Dynamic, nullptr,
+ * symmetric)  -- replaces quant.hpp:94-97 / quant.cpp:140-177 for the row
+ * groupings (one (s, z) per row), with an optional fused prologue and
+ * channel balance in front.
+ *   x       [dev] rows x cols of x_dtype, row pitch ldx elements
+ *   codes   [dev] rows x cols u8, row pitch ldc bytes
+ *   scale   [dev] rows f64 (QuantParams.scale)
+ *   zero    [dev] rows i32 (QuantParams.zero_point)
+ *   status  [dev] optional i32; |= 1 if any input is non-finite (the
+ *           reference throws std::invalid_argument; the stream-ordered API
+ *           reports it here instead of synchronising)
+ * bits in {2,4,6,8}.  Tie rounding is half-to-even (quant.cpp:9-16). */
+int dtq_quantize_rows(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx,
+                      int bits, int symmetric, int mode, const dtq_balance* balance,
+                      const dtq_prologue* prologue, uint8_t* codes, int64_t ldc,
+                      double* scale, int32_t* zero, int32_t* status, void* stream);
+
+/* ---------------------------------------------------------------- weights
+ * make_quant_linear (qgemm.cpp:9-21) on the device, with the weight side of
+ * apply_balance (W * diag(s), then the same rotation; balance.cpp:126-140,
+ * dtq_main.cpp:276-290) fused in front, all in fp64 as the reference.
+ *   w        [dev] N x K of w_dtype (F16/BF16/F32/F64), pitch ldw elements
+ *   bias     [dev] N f64 or NULL
+ *   balance  NULL or the layer's transform (copied into the handle; the
+ *            forward applies the activation side automatically)
+ * weight_bits in {4, 8}; act_bits in {2,4,6,8}.  W4 weights are stored
+ * packed (two codes per byte, trace_io.cpp:79-91 nibble order) and unpacked
+ * in shared memory by the GEMM. */
+int dtq_qlinear_create(const void* w, int w_dtype, int64_t N, int64_t K, int64_t ldw,
+                       int weight_bits, int act_bits, const double* bias,
+                       const dtq_balance* balance, void* stream, dtq_qlinear_t* out);
+
+/* Build from already-quantized weights (checkpoint loader path,
+ * trace_io.cpp:263-316): reference codes in [0, 2^b-1] with z = 2^(b-1).
+ *   codes   [dev] packed==0: N x K u8, pitch ld bytes
+ *                 packed==1: trace_io LSB-first bit stream of N*K codes
+ *   scale   [dev] N f64 */
+int dtq_qlinear_create_from_codes(const uint8_t* codes, int packed, int64_t ld,
+                                  int weight_bits, const double* scale, int64_t N, int64_t K,
+                                  int act_bits, const double* bias, const dtq_balance* balance,
+                                  void* stream, dtq_qlinear_t* out);
+
+int dtq_qlinear_destroy(dtq_qlinear_t h);
+
+int dtq_qlinear_info(dtq_qlinear_t h, int64_t* N, int64_t* K, int* weight_bits,
+                     int* act_bits);
+
+/* Copy the prepared weights back for inspection:
+ *   codes [host] N x K u8 reference codes (w_sym + z_w), scale [host] N f64,
+ *   wsum [host] N i32 (sum_c w_sym, qgemm.cpp:44-48).  Any may be NULL.
+ * Synchronises `stream`. */
+int dtq_qlinear_export(dtq_qlinear_t h, uint8_t* codes, double* scale, int32_t* wsum,
+                       void* stream);
+
+/* ---------------------------------------------------------------- GEMM
+ * qlinear_forward core (qgemm.cpp:52-63) on quantized activations:
+ *   codes [dev] M x K u8 with row pitch ldc (a multiple of 16 bytes)
+ *   s_x, z_x [dev] per-token params from dtq_quantize_rows
+ *   y [dev] M x N of y_dtype, pitch ldy elements:
+ *     F16 / BF16 / F32 : s_x*s_w*acc + bias, fp32 epilogue
+ *     S32              : acc - z_x*wsum (exact integer, for parity)
+ *     F64              : the reference's fp64 epilogue, bit-identical
+ *                        (uses an internal M x N s32 scratch)
+ * Fails with DTQ_ERR_OVERFLOW when (2^act_bits-1) * 2^(wbits-1) * K does
+ * not fit int32 (K > 65793 at W8A8), mirroring qgemm.cpp:29-34. */
+int dtq_qgemm(const uint8_t* codes, int64_t ldc, const double* s_x, const int32_t* z_x,
+              int64_t M, dtq_qlinear_t h, void* y, int y_dtype, int64_t ldy, void* stream);
+
+/* ---------------------------------------------------------------- fused layer
+ * Whole Matrix qlinear_forward(x, layer) (qgemm.cpp:23-67) on the device:
+ * fused quantizer (prologue + the handle's balance) then the GEMM.
+ * `workspace` [dev] of dtq_qlinear_workspace_bytes(h, M) bytes (codes and
+ * per-token params), or NULL to use a handle-owned buffer (not thread-safe
+ * per handle). */
+size_t dtq_qlinear_workspace_bytes(dtq_qlinear_t h, int64_t M);
+int dtq_qlinear_forward(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear_t h,
+                        int mode, const dtq_prologue* prologue, void* y, int y_dtype,
+                        int64_t ldy, void* workspace, size_t workspace_bytes,
+                        int32_t* status, void* stream);
+
+/* Same with HOST buffers (x [host] M x K dense, y [host] M x N dense):
+ * H2D copy, fused forward, D2H copy, stream synchronised before returning.
+ * Pinned host memory gives full PCIe/C2C bandwidth.  Non-finite input is
+ * reported as DTQ_ERR_INVALID_ARGUMENT (the reference's exception). */
+int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_t h, int mode,
+                             void* y, int y_dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DTQ_CAPI_H */

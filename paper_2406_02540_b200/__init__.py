@@ -1,0 +1,308 @@
+"""B200-native (sm_100a) ViDiT-Q quantized-linear path.
+
+Python front-end over the C ABI in include/dtq_capi.h, implemented by
+libdtq_b200.so (built in-tree from csrc/ by `python __graft_entry__.py` or
+`make -C paper_2406_02540_b200`).  PyTorch is used only for device memory
+and streams; every computation runs in the hand-written CUDA kernels.
+
+The names mirror the reference API (/root/reference/proj/core/include/dtq):
+
+  quantize_rows        quantize(x, per_token | per_output_channel, bits, Dynamic)
+  QuantLinear.create   make_quant_linear(w, weight_bits, act_bits, bias)
+                       (+ weight side of apply_balance)
+  QuantLinear.forward  qlinear_forward(x, layer) with the fused quantizer
+  QuantLinear.gemm     the integer GEMM + dequant epilogue on given codes
+  Balance              BalanceTransform{mask, rotation} (blockwise Hadamard)
+
+There is no CPU fallback: loading fails loudly without the built library,
+and every compute call fails without an sm_100 device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdtq_b200.so")
+
+F16, BF16, F32, F64, S32 = 0, 1, 2, 3, 4
+MODE_FAST, MODE_EXACT = 0, 1
+PROLOGUE_NONE, PROLOGUE_MODULATE, PROLOGUE_GELU, PROLOGUE_LN_MODULATE = 0, 1, 2, 3
+
+DTQ_OK, DTQ_ERR_INVALID_ARGUMENT, DTQ_ERR_OVERFLOW, DTQ_ERR_CUDA, DTQ_ERR_UNSUPPORTED = range(5)
+
+#: every symbol include/dtq_capi.h declares (checked by tests/test_capi.py)
+EXPORTED = (
+    "dtq_last_error", "dtq_capi_version", "dtq_device_check", "dtq_quantize_rows",
+    "dtq_qlinear_create", "dtq_qlinear_create_from_codes", "dtq_qlinear_destroy",
+    "dtq_qlinear_info", "dtq_qlinear_export", "dtq_qgemm", "dtq_qlinear_workspace_bytes",
+    "dtq_qlinear_forward", "dtq_qlinear_forward_host",
+)
+
+
+class DtqError(RuntimeError):
+    """DTQ_ERR_CUDA / DTQ_ERR_UNSUPPORTED."""
+
+
+class _Prologue(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("scale", C.c_void_p), ("shift", C.c_void_p),
+                ("eps", C.c_float)]
+
+
+class _Balance(C.Structure):
+    _fields_ = [("smooth", C.c_void_p), ("signs", C.c_void_p), ("hblock", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdtq_b200.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run `python __graft_entry__.py` "
+                          "(nvcc, sm_100a).  There is no CPU fallback.")
+    L = C.CDLL(LIB_PATH)
+    p, i64, i32 = C.c_void_p, C.c_int64, C.c_int
+    L.dtq_last_error.restype = C.c_char_p
+    L.dtq_quantize_rows.argtypes = [p, i32, i64, i64, i64, i32, i32, i32, p, p, p, i64, p, p, p, p]
+    L.dtq_qlinear_create.argtypes = [p, i32, i64, i64, i64, i32, i32, p, p, p, p]
+    L.dtq_qlinear_create_from_codes.argtypes = [p, i32, i64, i32, p, i64, i64, i32, p, p, p, p]
+    L.dtq_qlinear_destroy.argtypes = [p]
+    L.dtq_qlinear_info.argtypes = [p, p, p, p, p]
+    L.dtq_qlinear_export.argtypes = [p, p, p, p, p]
+    L.dtq_qgemm.argtypes = [p, i64, p, p, i64, p, p, i32, i64, p]
+    L.dtq_qlinear_workspace_bytes.restype = C.c_size_t
+    L.dtq_qlinear_workspace_bytes.argtypes = [p, i64]
+    L.dtq_qlinear_forward.argtypes = [p, i32, i64, i64, p, i32, p, p, i32, i64, p, C.c_size_t, p, p]
+    L.dtq_qlinear_forward_host.argtypes = [p, i32, i64, p, i32, p, i32, p]
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status == DTQ_OK:
+        return
+    msg = lib().dtq_last_error().decode(errors="replace")
+    if status == DTQ_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if status == DTQ_ERR_OVERFLOW:
+        raise OverflowError(msg)
+    raise DtqError(msg)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    return {torch.float16: F16, torch.bfloat16: BF16, torch.float32: F32, torch.float64: F64,
+            torch.int32: S32}[t]
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream=None) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+@dataclass
+class Balance:
+    """BalanceTransform (balance.hpp:31-34) on the device.
+
+    smooth: [K] fp64 ScalingMask.s (activations divided, weights multiplied)
+    signs:  [K] int8 +-1 RotationMatrix.sign_diag (blockwise, hblock columns)
+    """
+    smooth: Optional[object] = None
+    signs: Optional[object] = None
+    hblock: int = 128
+
+    def _c(self) -> _Balance:
+        return _Balance(_ptr(self.smooth), _ptr(self.signs), int(self.hblock))
+
+
+@dataclass
+class Prologue:
+    """Fused prologue: MODULATE x*(1+scale)+shift (toydit.cpp:339-369),
+    GELU (toydit.cpp:83) or LN_MODULATE (LayerNorm then modulate; unpinned)."""
+    kind: int = PROLOGUE_NONE
+    scale: Optional[object] = None   # [K] fp32 cuda
+    shift: Optional[object] = None   # [K] fp32 cuda
+    eps: float = 1e-6
+
+    def _c(self) -> _Prologue:
+        return _Prologue(self.kind, _ptr(self.scale), _ptr(self.shift), float(self.eps))
+
+
+def _ref_or_none(obj):
+    return None if obj is None else C.byref(obj)
+
+
+def quantize_rows(x, bits: int = 8, symmetric: bool = False, mode: int = MODE_FAST,
+                  balance: Optional[Balance] = None, prologue: Optional[Prologue] = None,
+                  status=None, stream=None):
+    """quantize(x, per_token, bits, Dynamic) on a CUDA tensor [rows, cols].
+
+    Returns (codes u8 [rows, cols], scale f64 [rows], zero_point i32 [rows])."""
+    torch = _torch()
+    assert x.is_cuda and x.dim() == 2 and x.stride(1) == 1
+    rows, cols = x.shape
+    ldc = (cols + 15) // 16 * 16
+    codes_buf = torch.empty((rows, ldc), dtype=torch.uint8, device=x.device)
+    scale = torch.empty(rows, dtype=torch.float64, device=x.device)
+    zero = torch.empty(rows, dtype=torch.int32, device=x.device)
+    b = balance._c() if balance is not None else None
+    pr = prologue._c() if prologue is not None else None
+    _check(lib().dtq_quantize_rows(x.data_ptr(), _dtype_code(x.dtype), rows, cols, x.stride(0),
+                                   bits, int(symmetric), mode, _ref_or_none(b), _ref_or_none(pr),
+                                   codes_buf.data_ptr(), ldc, scale.data_ptr(), zero.data_ptr(),
+                                   _ptr(status), _stream(stream)))
+    return codes_buf[:, :cols], scale, zero
+
+
+class QuantLinear:
+    """Device-resident QuantLinear (qgemm.hpp:17-24) behind an opaque handle."""
+
+    def __init__(self, handle: int, N: int, K: int, wbits: int, abits: int, balance=None):
+        self._h = C.c_void_p(handle)
+        self.N, self.K, self.weight_bits, self.act_bits = N, K, wbits, abits
+        self.balance = balance
+        self._ws = None
+
+    @classmethod
+    def create(cls, w, weight_bits: int = 8, act_bits: int = 8, bias=None,
+               balance: Optional[Balance] = None, stream=None) -> "QuantLinear":
+        """make_quant_linear (qgemm.cpp:9-21) + weight-side balance, on the GPU."""
+        torch = _torch()
+        assert w.is_cuda and w.dim() == 2 and w.stride(1) == 1
+        N, K = w.shape
+        bias_t = None if bias is None else torch.as_tensor(bias, dtype=torch.float64,
+                                                           device=w.device).contiguous()
+        h = C.c_void_p()
+        b = balance._c() if balance is not None else None
+        _check(lib().dtq_qlinear_create(w.data_ptr(), _dtype_code(w.dtype), N, K, w.stride(0),
+                                        weight_bits, act_bits, _ptr(bias_t), _ref_or_none(b),
+                                        _stream(stream), C.byref(h)))
+        return cls(h.value, N, K, weight_bits, act_bits, balance)
+
+    @classmethod
+    def from_codes(cls, codes, scale, weight_bits: int, K: int, act_bits: int = 8, bias=None,
+                   packed: bool = False, balance: Optional[Balance] = None, stream=None):
+        """Build from reference codes (checkpoint loader path, trace_io.cpp:263-316)."""
+        torch = _torch()
+        N = scale.shape[0]
+        bias_t = None if bias is None else torch.as_tensor(bias, dtype=torch.float64,
+                                                           device=codes.device).contiguous()
+        ld = 0 if packed else codes.stride(0)
+        h = C.c_void_p()
+        b = balance._c() if balance is not None else None
+        _check(lib().dtq_qlinear_create_from_codes(codes.data_ptr(), int(packed), ld, weight_bits,
+                                                   scale.data_ptr(), N, K, act_bits, _ptr(bias_t),
+                                                   _ref_or_none(b), _stream(stream), C.byref(h)))
+        return cls(h.value, N, K, weight_bits, act_bits, balance)
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib().dtq_qlinear_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def export(self):
+        """(codes u8 [N,K], scale f64 [N], wsum i32 [N]) as numpy, reference convention."""
+        import numpy as np
+        codes = np.zeros((self.N, self.K), np.uint8)
+        scale = np.zeros(self.N, np.float64)
+        wsum = np.zeros(self.N, np.int32)
+        _check(lib().dtq_qlinear_export(self._h, codes.ctypes.data, scale.ctypes.data,
+                                        wsum.ctypes.data, _stream(None)))
+        return codes, scale, wsum
+
+    def workspace(self, M: int, device=None):
+        torch = _torch()
+        n = lib().dtq_qlinear_workspace_bytes(self._h, M)
+        return torch.empty(n, dtype=torch.uint8, device=device or "cuda")
+
+    def gemm(self, codes, s_x, z_x, out_dtype=None, out=None, stream=None):
+        """Integer GEMM + epilogue on quantized activations (qgemm.cpp:52-63)."""
+        torch = _torch()
+        M = codes.shape[0]
+        if out is None:
+            out = torch.empty((M, self.N), dtype=out_dtype or torch.float16, device=codes.device)
+        _check(lib().dtq_qgemm(codes.data_ptr(), codes.stride(0), s_x.data_ptr(), z_x.data_ptr(),
+                               M, self._h, out.data_ptr(), _dtype_code(out.dtype), out.stride(0),
+                               _stream(stream)))
+        return out
+
+    def forward(self, x, out_dtype=None, mode: int = MODE_FAST,
+                prologue: Optional[Prologue] = None, out=None, workspace=None, status=None,
+                stream=None):
+        """qlinear_forward(x, layer): fused quantizer + GEMM, stream-ordered."""
+        torch = _torch()
+        M = x.shape[0]
+        if out is None:
+            out = torch.empty((M, self.N), dtype=out_dtype or torch.float16, device=x.device)
+        pr = prologue._c() if prologue is not None else None
+        ws_ptr, ws_n = (None, 0) if workspace is None else (workspace.data_ptr(), workspace.numel())
+        _check(lib().dtq_qlinear_forward(x.data_ptr(), _dtype_code(x.dtype), M, x.stride(0),
+                                         self._h, mode, _ref_or_none(pr), out.data_ptr(),
+                                         _dtype_code(out.dtype), out.stride(0), ws_ptr, ws_n,
+                                         _ptr(status), _stream(stream)))
+        return out
+
+    def forward_host(self, x_host, y_host, mode: int = MODE_FAST, stream=None):
+        """Host buffers in, host buffers out (H2D + forward + D2H, synchronised)."""
+        torch = _torch()
+        assert not x_host.is_cuda and not y_host.is_cuda
+        M = x_host.shape[0]
+        _check(lib().dtq_qlinear_forward_host(x_host.data_ptr(), _dtype_code(x_host.dtype), M,
+                                              self._h, mode, y_host.data_ptr(),
+                                              _dtype_code(y_host.dtype), _stream(stream)))
+        return y_host
+
+
+def hadamard_signs(n: int, seed: int, randomize: bool = True):
+    """RotationMatrix.sign_diag (balance.cpp:73-78): first n draws of
+    std::mt19937_64(seed), (draw & 1) ? +1 : -1, as an int8 numpy array.
+    (Host-side, one-time; the engine is the C++ standard's mt19937_64.)"""
+    import numpy as np
+    out = np.ones(n, np.int8)
+    if not randomize:
+        return out
+    mt = [0] * 312
+    mt[0] = seed & 0xFFFFFFFFFFFFFFFF
+    for i in range(1, 312):
+        mt[i] = (6364136223846793005 * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i) & 0xFFFFFFFFFFFFFFFF
+    idx = 312
+    UM, LM = 0xFFFFFFFF80000000, 0x7FFFFFFF
+    for k in range(n):
+        if idx >= 312:
+            for i in range(312):
+                x = (mt[i] & UM) | (mt[(i + 1) % 312] & LM)
+                xa = x >> 1
+                if x & 1:
+                    xa ^= 0xB5026F5AA96619E9
+                mt[i] = mt[(i + 156) % 312] ^ xa
+            idx = 0
+        y = mt[idx]
+        idx += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        out[k] = 1 if (y & 1) else -1
+    return out

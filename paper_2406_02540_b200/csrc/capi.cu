@@ -1,0 +1,763 @@
+// capi.cu -- implementation of include/dtq_capi.h on sm_100a.
+//
+// Host-side plumbing only: argument validation with the reference's error
+// conventions, handle management (the prepared QuantLinear lives in HBM),
+// TMA descriptor encoding, kernel selection and launch.  All arithmetic is
+// in fused_quant.cuh (activation / weight quantizer) and qgemm_sm100.cuh
+// (tcgen05 integer GEMM).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/dtq_capi.h"
+#include "launch.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(DTQ_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                  \
+  } while (0)
+
+#define DTQ_TRY(expr)          \
+  do {                         \
+    int st_ = (expr);          \
+    if (st_ != DTQ_OK) return st_; \
+  } while (0)
+
+bool bits_supported(int b) { return b == 2 || b == 4 || b == 6 || b == 8; }
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+struct DeviceInfo {
+  int dev = -1;
+  int sms = 0;
+  int major = 0;
+};
+
+DeviceInfo& device_info() {
+  thread_local DeviceInfo info;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return info;
+  if (info.dev != dev) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, dev) == cudaSuccess) {
+      info.dev = dev;
+      info.sms = p.multiProcessorCount;
+      info.major = p.major;
+    }
+  }
+  return info;
+}
+
+int check_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return fail(DTQ_ERR_CUDA, "no CUDA device (the sm_100a path has no CPU fallback)");
+  DeviceInfo& d = device_info();
+  if (d.major != 10)
+    return fail(DTQ_ERR_CUDA, "device compute capability %d.x is not sm_100 (B200)", d.major);
+  return DTQ_OK;
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------------------------ TMA maps
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000,
+                                         cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D u8 tensor [rows, cols] with row pitch `ld` bytes, box {box_cols, box_rows}.
+int make_tmap_u8(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                 int box_cols, int box_rows, CUtensorMapSwizzle swz) {
+  auto fn = encode_fn();
+  if (!fn) return fail(DTQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0 || ld % 16 != 0)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "TMA operand needs 16-byte aligned base and pitch");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DTQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return DTQ_OK;
+}
+
+// ------------------------------------------------------------------ FQ launch
+// (kernel instantiations live in fq_kernels.cu so they compile in parallel)
+int launch_fq(const dtq_fq::FqArgs& a, int x_dtype, bool exact, int cpt, bool vec, int block,
+              cudaStream_t st) {
+  int sms = device_info().sms;
+  cudaError_t e = dtq_launch_fq(a, x_dtype, exact, cpt, vec, block, sms, st);
+  if (e != cudaSuccess) return fail(DTQ_ERR_CUDA, "fused quantizer launch: %s", cudaGetErrorString(e));
+  return DTQ_OK;
+}
+
+size_t dtype_size(int dt) {
+  switch (dt) {
+    case DTQ_F16:
+    case DTQ_BF16:
+      return 2;
+    case DTQ_F32:
+    case DTQ_S32:
+      return 4;
+    case DTQ_F64:
+      return 8;
+  }
+  return 0;
+}
+
+// Row quantizer; `smooth_mul` selects W * s (weight side) instead of X / s.
+int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx,
+                       int bits, int symmetric, int mode, int smooth_mul, const double* smooth_d,
+                       const float* inv_smooth_f, const int8_t* signs, int hblock,
+                       const dtq_prologue* pro, uint8_t* codes, int64_t ldc, double* scale,
+                       int32_t* zero, int32_t* status, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: empty matrix");
+  if (!bits_supported(bits))
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: bits must be one of {2,4,6,8}");
+  if (ldx < cols || ldc < cols) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: pitch < cols");
+  if (!x || !codes || !scale || !zero)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: null pointer");
+  if (dtype_size(x_dtype) == 0 || x_dtype == DTQ_S32)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: bad input dtype %d", x_dtype);
+  if (signs) {
+    if (hblock < 8 || hblock > 256 || (hblock & (hblock - 1)) != 0)
+      return fail(DTQ_ERR_INVALID_ARGUMENT,
+                  "hadamard: block must be a power of two in [8, 256]");
+    if (cols % hblock != 0)
+      return fail(DTQ_ERR_INVALID_ARGUMENT, "rotate_channels: channel count %lld not a multiple "
+                  "of the rotation block %d", (long long)cols, hblock);
+  }
+  if (cols > 16384) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: cols > 16384");
+  const int kind = pro ? pro->kind : DTQ_PROLOGUE_NONE;
+  if (kind < 0 || kind > 3) return fail(DTQ_ERR_INVALID_ARGUMENT, "bad prologue kind");
+  if ((kind == DTQ_PROLOGUE_MODULATE || kind == DTQ_PROLOGUE_LN_MODULATE) &&
+      (!pro->scale || !pro->shift))
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "modulate prologue needs scale and shift");
+  DTQ_TRY(check_device());
+
+  const bool exact = mode == DTQ_MODE_EXACT || x_dtype == DTQ_F64;
+  const int64_t chunks = (cols + 7) / 8;
+  const int cpt = chunks <= 1024 ? 1 : 8;
+  const int64_t align = signs ? (hblock / 8 > 16 ? hblock / 8 : 16) : 16;
+  const int64_t tpr = round_up((chunks + cpt - 1) / cpt, align);
+  if (tpr > (cpt == 1 ? 1024 : 256))
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: cols too large");
+  const int block = static_cast<int>(round_up(tpr, 32));
+  const size_t es = dtype_size(x_dtype);
+  const bool vec = cols % 8 == 0 && (ldx * es) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(x) % 16 == 0 && ldc % 8 == 0 &&
+                   reinterpret_cast<uintptr_t>(codes) % 8 == 0 &&
+                   (!smooth_d || reinterpret_cast<uintptr_t>(smooth_d) % 16 == 0) &&
+                   (!inv_smooth_f || reinterpret_cast<uintptr_t>(inv_smooth_f) % 16 == 0) &&
+                   (kind == 0 || kind == 2 ||
+                    (reinterpret_cast<uintptr_t>(pro->scale) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(pro->shift) % 16 == 0));
+
+  dtq_fq::FqArgs a{};
+  a.x = x;
+  a.M = rows;
+  a.K = cols;
+  a.ldx = ldx;
+  a.codes = codes;
+  a.ldc = ldc;
+  a.scale = scale;
+  a.zero = zero;
+  a.bits = bits;
+  a.symmetric = symmetric;
+  a.smooth_d = exact ? smooth_d : nullptr;
+  a.inv_smooth_f = exact ? nullptr : inv_smooth_f;
+  if (!exact && smooth_mul)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "weight-side smoothing runs in exact mode only");
+  if (exact && !smooth_d && inv_smooth_f)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "exact mode needs the fp64 smoothing vector");
+  if (!exact && smooth_d && !inv_smooth_f)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "fast mode needs the fp32 reciprocal smoothing vector");
+  a.signs = signs;
+  a.hblock = signs ? hblock : 0;
+  a.pro_scale = pro ? pro->scale : nullptr;
+  a.pro_shift = pro ? pro->shift : nullptr;
+  a.eps = pro ? pro->eps : 0.f;
+  a.status = status;
+  a.pro = kind;
+  a.smooth_mul = smooth_mul;
+  a.tpr = static_cast<int>(tpr);
+
+  return launch_fq(a, x_dtype, exact, cpt, vec, block, st);
+}
+
+// ------------------------------------------------------------------ weight prep kernels
+// reference codes (z = 2^(b-1)) -> s8 w_sym rows (W8) or packed nibbles (W4),
+// plus w_row_sum (qgemm.cpp:40-49).  One CTA per output channel.
+__global__ void weight_pack_kernel(const uint8_t* __restrict__ codes, int64_t ldc, int64_t N,
+                                   int64_t K, int wbits, int8_t* __restrict__ w8, int64_t ld8,
+                                   uint8_t* __restrict__ w4, int64_t ld4,
+                                   int32_t* __restrict__ wsum) {
+  const int64_t o = blockIdx.x;
+  if (o >= N) return;
+  const int32_t z = 1 << (wbits - 1);
+  int32_t sum = 0;
+  if (wbits == 8) {
+    for (int64_t c = threadIdx.x; c < ld8; c += blockDim.x) {
+      int32_t v = 0;
+      if (c < K) v = static_cast<int32_t>(codes[o * ldc + c]) - z;
+      w8[o * ld8 + c] = static_cast<int8_t>(v);
+      sum += v;
+    }
+  } else {
+    for (int64_t b = threadIdx.x; b < ld4; b += blockDim.x) {
+      const int64_t c0 = 2 * b, c1 = 2 * b + 1;
+      const uint32_t lo = c0 < K ? codes[o * ldc + c0] : 8u;  // pad: code 8 -> w_sym 0
+      const uint32_t hi = c1 < K ? codes[o * ldc + c1] : 8u;
+      w4[o * ld4 + b] = static_cast<uint8_t>(lo | (hi << 4));
+      sum += static_cast<int32_t>(lo) - 8 + static_cast<int32_t>(hi) - 8;
+    }
+  }
+  __shared__ int32_t red[32];
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t s = 0;
+    for (int i = 0; i < (blockDim.x + 31) / 32; ++i) s += red[i];
+    wsum[o] = s;
+  }
+}
+
+// trace_io LSB-first bit stream -> one code per byte (unpack_codes, trace_io.cpp:93-109)
+__global__ void unpack_stream_kernel(const uint8_t* __restrict__ bytes, int64_t count, int bits,
+                                     int64_t N, int64_t K, uint8_t* __restrict__ out,
+                                     int64_t ldo) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t bitpos = i * bits;
+    uint32_t v = bytes[bitpos / 8] >> (bitpos % 8);
+    if (bitpos % 8 + bits > 8) v |= static_cast<uint32_t>(bytes[bitpos / 8 + 1]) << (8 - bitpos % 8);
+    out[(i / K) * ldo + (i % K)] = static_cast<uint8_t>(v & ((1u << bits) - 1));
+  }
+}
+
+__global__ void export_codes_kernel(const int8_t* __restrict__ w8, int64_t ld8,
+                                    const uint8_t* __restrict__ w4, int64_t ld4, int wbits,
+                                    int64_t N, int64_t K, uint8_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N * K;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t o = i / K, c = i % K;
+    if (wbits == 8)
+      out[i] = static_cast<uint8_t>(static_cast<int32_t>(w8[o * ld8 + c]) + 128);
+    else
+      out[i] = (w4[o * ld4 + c / 2] >> (4 * (c & 1))) & 0xF;
+  }
+}
+
+// fp64 parity epilogue (qgemm.cpp:61-63 operation order):
+//   y = s_x[t] * s_w[o] * (double)acc + bias[o]
+__global__ void parity_epilogue_kernel(const int32_t* __restrict__ acc, int64_t M, int64_t N,
+                                       const double* __restrict__ s_x,
+                                       const double* __restrict__ s_w,
+                                       const double* __restrict__ bias, double* __restrict__ y,
+                                       int64_t ldy) {
+  const int64_t total = M * N;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / N, o = i % N;
+    // explicit roundings: no FMA contraction, same as the reference's x86 build
+    double out = __dmul_rn(__dmul_rn(s_x[t], s_w[o]), static_cast<double>(acc[i]));
+    if (bias) out = __dadd_rn(out, bias[o]);
+    y[t * ldy + o] = out;
+  }
+}
+
+__global__ void to_f32_kernel(const double* __restrict__ in, float* __restrict__ out, int64_t n,
+                              int reciprocal) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<float>(reciprocal ? 1.0 / in[i] : in[i]);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ handle
+struct dtq_qlinear_s {
+  int64_t N = 0, K = 0;
+  int wbits = 8, abits = 8;
+  int8_t* w8 = nullptr;   // [N, ld8] s8 (W8)
+  int64_t ld8 = 0;
+  uint8_t* w4 = nullptr;  // [N, ld4] packed nibbles, raw codes (W4)
+  int64_t ld4 = 0;
+  double* s_w = nullptr;      // [N]
+  float* s_w_f = nullptr;     // [N]
+  int32_t* wsum = nullptr;    // [N]
+  double* bias = nullptr;     // [N] or null
+  float* bias_f = nullptr;    // [N] or null
+  double* smooth = nullptr;   // [K] or null
+  float* inv_smooth = nullptr;
+  int8_t* signs = nullptr;    // [K] or null
+  int hblock = 0;
+  CUtensorMap tmB;
+  // handle-owned scratch (forward without workspace, F64 output, host forward)
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  int32_t* acc32 = nullptr;
+  size_t acc32_bytes = 0;
+  void* hx = nullptr;
+  size_t hx_bytes = 0;
+  void* hy = nullptr;
+  size_t hy_bytes = 0;
+  int32_t* status = nullptr;
+};
+
+namespace {
+
+int grow(void** p, size_t* cur, size_t need) {
+  if (*cur >= need) return DTQ_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cur = 0;
+  CUDA_TRY(cudaMalloc(p, need));
+  *cur = need;
+  return DTQ_OK;
+}
+
+void free_handle(dtq_qlinear_s* h) {
+  void* ptrs[] = {h->w8, h->w4, h->s_w, h->s_w_f, h->wsum, h->bias, h->bias_f, h->smooth,
+                  h->inv_smooth, h->signs, h->scratch, h->acc32, h->hx, h->hy, h->status};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete h;
+}
+
+int alloc_status(dtq_qlinear_s* h, cudaStream_t st) {
+  CUDA_TRY(cudaMalloc(&h->status, sizeof(int32_t)));
+  CUDA_TRY(cudaMemsetAsync(h->status, 0, sizeof(int32_t), st));
+  return DTQ_OK;
+}
+
+int copy_balance(dtq_qlinear_s* h, const dtq_balance* bal, cudaStream_t st) {
+  if (!bal) return DTQ_OK;
+  const int64_t K = h->K;
+  if (bal->smooth) {
+    CUDA_TRY(cudaMalloc(&h->smooth, K * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&h->inv_smooth, K * sizeof(float)));
+    CUDA_TRY(cudaMemcpyAsync(h->smooth, bal->smooth, K * sizeof(double),
+                             cudaMemcpyDeviceToDevice, st));
+    to_f32_kernel<<<static_cast<int>((K + 255) / 256), 256, 0, st>>>(h->smooth, h->inv_smooth,
+                                                                      K, 1);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (bal->signs) {
+    if (bal->hblock < 8 || bal->hblock > 256 || (bal->hblock & (bal->hblock - 1)) != 0)
+      return fail(DTQ_ERR_INVALID_ARGUMENT, "hadamard: block must be a power of two in [8, 256]");
+    if (K % bal->hblock != 0)
+      return fail(DTQ_ERR_INVALID_ARGUMENT, "rotate_channels: K not a multiple of the block");
+    CUDA_TRY(cudaMalloc(&h->signs, K));
+    CUDA_TRY(cudaMemcpyAsync(h->signs, bal->signs, K, cudaMemcpyDeviceToDevice, st));
+    h->hblock = bal->hblock;
+  }
+  return DTQ_OK;
+}
+
+int overflow_check(int abits, int wbits, int64_t K) {
+  // int32 accumulation must be exact: (2^ab - 1) * 2^(wb-1) * K < 2^31
+  const int64_t max_term = static_cast<int64_t>((1 << abits) - 1) * (int64_t{1} << (wbits - 1));
+  if (max_term * K > INT32_MAX)
+    return fail(DTQ_ERR_OVERFLOW, "qlinear_forward: accumulator could overflow (K=%lld)",
+                (long long)K);
+  return DTQ_OK;
+}
+
+// codes [N, ldc] (reference convention) + scale [N] -> handle weights
+int finish_from_codes(dtq_qlinear_s* h, const uint8_t* codes, int64_t ldc, const double* scale,
+                      const double* bias, cudaStream_t st) {
+  const int64_t N = h->N, K = h->K;
+  if (h->wbits == 8) {
+    h->ld8 = round_up(K, 16);
+    CUDA_TRY(cudaMalloc(&h->w8, N * h->ld8));
+  } else {
+    h->ld4 = round_up((K + 1) / 2, 16);
+    CUDA_TRY(cudaMalloc(&h->w4, N * h->ld4));
+  }
+  CUDA_TRY(cudaMalloc(&h->wsum, N * sizeof(int32_t)));
+  weight_pack_kernel<<<static_cast<int>(N), 256, 0, st>>>(codes, ldc, N, K, h->wbits, h->w8,
+                                                          h->ld8, h->w4, h->ld4, h->wsum);
+  CUDA_TRY(cudaGetLastError());
+  if (scale != h->s_w) {
+    CUDA_TRY(cudaMalloc(&h->s_w, N * sizeof(double)));
+    CUDA_TRY(cudaMemcpyAsync(h->s_w, scale, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  CUDA_TRY(cudaMalloc(&h->s_w_f, N * sizeof(float)));
+  const int g = static_cast<int>((N + 255) / 256);
+  to_f32_kernel<<<g, 256, 0, st>>>(h->s_w, h->s_w_f, N, 0);
+  CUDA_TRY(cudaGetLastError());
+  if (bias) {
+    CUDA_TRY(cudaMalloc(&h->bias, N * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&h->bias_f, N * sizeof(float)));
+    CUDA_TRY(cudaMemcpyAsync(h->bias, bias, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    to_f32_kernel<<<g, 256, 0, st>>>(h->bias, h->bias_f, N, 0);
+    CUDA_TRY(cudaGetLastError());
+  }
+  const int BN = N > 128 ? 256 : 128;
+  if (h->wbits == 8)
+    DTQ_TRY(make_tmap_u8(&h->tmB, h->w8, N, K, h->ld8, dtq_gemm::BK, BN,
+                         CU_TENSOR_MAP_SWIZZLE_128B));
+  else
+    DTQ_TRY(make_tmap_u8(&h->tmB, h->w4, N, (K + 1) / 2, h->ld4, dtq_gemm::BK / 2, BN,
+                         CU_TENSOR_MAP_SWIZZLE_NONE));
+  return DTQ_OK;
+}
+
+// ------------------------------------------------------------------ GEMM launch
+// (kernel instantiations live in gemm_w8.cu / gemm_w4.cu)
+int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32_t* z_x,
+               int64_t M, dtq_qlinear_s* h, void* y, int y_dtype, int64_t ldy, cudaStream_t st) {
+  if (!h) return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: null handle");
+  if (M <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: M must be >= 1");
+  if (!codes || !s_x || !z_x || !y) return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: null pointer");
+  if (ldy < h->N) return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: ldy < N");
+  if (M > INT32_MAX / 2) return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: M too large");
+  DTQ_TRY(overflow_check(h->abits, h->wbits, h->K));
+  DTQ_TRY(check_device());
+  const int BN = h->N > 128 ? 256 : 128;
+
+  CUtensorMap tA;
+  DTQ_TRY(make_tmap_u8(&tA, codes, M, h->K, ldc, dtq_gemm::BK, dtq_gemm::BM,
+                       CU_TENSOR_MAP_SWIZZLE_128B));
+
+  void* yk = y;
+  int64_t ldk = ldy;
+  int kind;
+  switch (y_dtype) {
+    case DTQ_F16: kind = dtq_gemm::kOutF16; break;
+    case DTQ_BF16: kind = dtq_gemm::kOutBF16; break;
+    case DTQ_F32: kind = dtq_gemm::kOutF32; break;
+    case DTQ_S32: kind = dtq_gemm::kOutS32; break;
+    case DTQ_F64:
+      kind = dtq_gemm::kOutS32;
+      DTQ_TRY(grow(reinterpret_cast<void**>(&h->acc32), &h->acc32_bytes,
+                   static_cast<size_t>(M) * h->N * sizeof(int32_t)));
+      yk = h->acc32;
+      ldk = h->N;
+      break;
+    default: return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: bad output dtype %d", y_dtype);
+  }
+  const size_t es = kind == dtq_gemm::kOutF16 || kind == dtq_gemm::kOutBF16 ? 2 : 4;
+
+  dtq_gemm::GemmArgs g{};
+  g.M = static_cast<int>(M);
+  g.N = static_cast<int>(h->N);
+  g.K = static_cast<int>(h->K);
+  g.tiles_m = static_cast<int>((M + dtq_gemm::BM - 1) / dtq_gemm::BM);
+  g.tiles_n = static_cast<int>((h->N + BN - 1) / BN);
+  g.k_blocks = static_cast<int>((h->K + dtq_gemm::BK - 1) / dtq_gemm::BK);
+  g.s_x = s_x;
+  g.z_x = z_x;
+  g.s_w = h->s_w_f;
+  g.wsum = h->wsum;
+  g.bias = kind == dtq_gemm::kOutS32 ? nullptr : h->bias_f;
+  g.y = yk;
+  g.ldy = ldk;
+  g.out_kind = kind;
+  g.vec_store = (reinterpret_cast<uintptr_t>(yk) % 16 == 0) && ((ldk * es) % 16 == 0);
+
+  const int sms = device_info().sms;
+  const cudaError_t e = h->wbits == 8 ? dtq_launch_gemm_w8(tA, h->tmB, g, BN, sms, st)
+                                      : dtq_launch_gemm_w4(tA, h->tmB, g, BN, sms, st);
+  if (e != cudaSuccess) return fail(DTQ_ERR_CUDA, "qgemm launch: %s", cudaGetErrorString(e));
+
+  if (y_dtype == DTQ_F64) {
+    const int64_t total = M * h->N;
+    const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+    parity_epilogue_kernel<<<grid, 256, 0, st>>>(
+        h->acc32, M, h->N, s_x, h->s_w, h->bias, static_cast<double*>(y), ldy);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return DTQ_OK;
+}
+
+size_t ws_layout(const dtq_qlinear_s* h, int64_t M, int64_t* ldc, size_t* off_s, size_t* off_z) {
+  *ldc = round_up(h->K, 16);
+  const size_t codes = round_up(static_cast<int64_t>(M) * *ldc, 256);
+  *off_s = codes;
+  *off_z = codes + round_up(M * 8, 256);
+  return *off_z + round_up(M * 4, 256);
+}
+
+int forward_impl(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear_s* h, int mode,
+                 const dtq_prologue* pro, void* y, int y_dtype, int64_t ldy, void* ws,
+                 size_t ws_bytes, int32_t* status, cudaStream_t st) {
+  if (!h) return fail(DTQ_ERR_INVALID_ARGUMENT, "forward: null handle");
+  if (ldx < h->K) return fail(DTQ_ERR_INVALID_ARGUMENT, "qlinear_forward: X cols != C_in");
+  int64_t ldc;
+  size_t off_s, off_z;
+  const size_t need = ws_layout(h, M, &ldc, &off_s, &off_z);
+  if (!ws) {
+    DTQ_TRY(grow(&h->scratch, &h->scratch_bytes, need));
+    ws = h->scratch;
+  } else if (ws_bytes < need) {
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "forward: workspace too small (%zu < %zu)", ws_bytes,
+                need);
+  }
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  uint8_t* codes = base;
+  double* s_x = reinterpret_cast<double*>(base + off_s);
+  int32_t* z_x = reinterpret_cast<int32_t*>(base + off_z);
+  DTQ_TRY(overflow_check(h->abits, h->wbits, h->K));
+  DTQ_TRY(quantize_rows_impl(x, x_dtype, M, h->K, ldx, h->abits, 0, mode, 0, h->smooth,
+                             h->inv_smooth, h->signs, h->hblock, pro, codes, ldc, s_x, z_x,
+                             status, st));
+  return qgemm_impl(codes, ldc, s_x, z_x, M, h, y, y_dtype, ldy, st);
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* dtq_last_error(void) { return g_last_error.c_str(); }
+
+int dtq_capi_version(void) { return DTQ_CAPI_VERSION; }
+
+int dtq_device_check(void) { return check_device(); }
+
+int dtq_quantize_rows(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx,
+                      int bits, int symmetric, int mode, const dtq_balance* balance,
+                      const dtq_prologue* prologue, uint8_t* codes, int64_t ldc, double* scale,
+                      int32_t* zero, int32_t* status, void* stream) {
+  const double* smooth = balance ? balance->smooth : nullptr;
+  cudaStream_t st = as_stream(stream);
+  float* inv = nullptr;
+  const bool exact = mode == DTQ_MODE_EXACT || x_dtype == DTQ_F64;
+  if (smooth && !exact) {
+    // fast mode multiplies by fp32 reciprocals: derive them stream-ordered
+    if (cols <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: empty matrix");
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&inv), cols * sizeof(float), st));
+    to_f32_kernel<<<static_cast<int>((cols + 255) / 256), 256, 0, st>>>(smooth, inv, cols, 1);
+    CUDA_TRY(cudaGetLastError());
+  }
+  const int r = quantize_rows_impl(x, x_dtype, rows, cols, ldx, bits, symmetric, mode, 0,
+                                   exact ? smooth : nullptr, inv,
+                                   balance ? balance->signs : nullptr,
+                                   balance ? balance->hblock : 0, prologue, codes, ldc, scale,
+                                   zero, status, st);
+  if (inv) cudaFreeAsync(inv, st);
+  return r;
+}
+
+int dtq_qlinear_create(const void* w, int w_dtype, int64_t N, int64_t K, int64_t ldw,
+                       int weight_bits, int act_bits, const double* bias,
+                       const dtq_balance* balance, void* stream, dtq_qlinear_t* out) {
+  if (!out) return fail(DTQ_ERR_INVALID_ARGUMENT, "create: null out");
+  *out = nullptr;
+  if (weight_bits != 8 && weight_bits != 4)
+    return fail(weight_bits == 2 || weight_bits == 6 ? DTQ_ERR_UNSUPPORTED : DTQ_ERR_INVALID_ARGUMENT,
+                "make_quant_linear: device GEMM supports weight_bits 4 and 8 (got %d)", weight_bits);
+  if (!bits_supported(act_bits))
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "make_quant_linear: unsupported bit width");
+  if (N <= 0 || K <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "make_quant_linear: empty W");
+  DTQ_TRY(check_device());
+  cudaStream_t st = as_stream(stream);
+  auto* h = new dtq_qlinear_s();
+  h->N = N;
+  h->K = K;
+  h->wbits = weight_bits;
+  h->abits = act_bits;
+  int r = alloc_status(h, st);
+  if (r == DTQ_OK) r = copy_balance(h, balance, st);
+  uint8_t* codes = nullptr;
+  if (r == DTQ_OK) {
+    const int64_t ldc = round_up(K, 16);
+    if (cudaMalloc(&codes, N * ldc) != cudaSuccess ||
+        cudaMalloc(&h->s_w, N * sizeof(double)) != cudaSuccess) {
+      r = fail(DTQ_ERR_CUDA, "create: out of device memory");
+    } else {
+      int32_t* zw = nullptr;
+      if (cudaMalloc(&zw, N * sizeof(int32_t)) != cudaSuccess) {
+        r = fail(DTQ_ERR_CUDA, "create: out of device memory");
+      } else {
+        // weight side of apply_balance: W * s then the rotation, in fp64; then
+        // symmetric per-output-channel quantization (make_quant_linear)
+        r = quantize_rows_impl(w, w_dtype, N, K, ldw, weight_bits, 1, DTQ_MODE_EXACT, 1,
+                               h->smooth, nullptr, h->signs, h->hblock, nullptr, codes, ldc,
+                               h->s_w, zw, h->status, st);
+        if (r == DTQ_OK) {
+          int32_t bad = 0;
+          if (cudaMemcpyAsync(&bad, h->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st) !=
+                  cudaSuccess ||
+              cudaStreamSynchronize(st) != cudaSuccess)
+            r = fail(DTQ_ERR_CUDA, "create: status readback failed");
+          else if (bad)
+            r = fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: non-finite value in group");
+        }
+        cudaFreeAsync(zw, st);
+      }
+      if (r == DTQ_OK) r = finish_from_codes(h, codes, ldc, h->s_w, bias, st);
+    }
+  }
+  if (codes) cudaFreeAsync(codes, st);
+  if (r != DTQ_OK) {
+    free_handle(h);
+    return r;
+  }
+  *out = h;
+  return DTQ_OK;
+}
+
+int dtq_qlinear_create_from_codes(const uint8_t* codes, int packed, int64_t ld, int weight_bits,
+                                  const double* scale, int64_t N, int64_t K, int act_bits,
+                                  const double* bias, const dtq_balance* balance, void* stream,
+                                  dtq_qlinear_t* out) {
+  if (!out) return fail(DTQ_ERR_INVALID_ARGUMENT, "create: null out");
+  *out = nullptr;
+  if (weight_bits != 8 && weight_bits != 4)
+    return fail(DTQ_ERR_UNSUPPORTED, "device GEMM supports weight_bits 4 and 8");
+  if (!bits_supported(act_bits)) return fail(DTQ_ERR_INVALID_ARGUMENT, "unsupported bit width");
+  if (N <= 0 || K <= 0 || !codes || !scale)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "create_from_codes: bad arguments");
+  if (!packed && ld < K) return fail(DTQ_ERR_INVALID_ARGUMENT, "create_from_codes: ld < K");
+  DTQ_TRY(check_device());
+  cudaStream_t st = as_stream(stream);
+  auto* h = new dtq_qlinear_s();
+  h->N = N;
+  h->K = K;
+  h->wbits = weight_bits;
+  h->abits = act_bits;
+  int r = alloc_status(h, st);
+  if (r == DTQ_OK) r = copy_balance(h, balance, st);
+  uint8_t* tmp = nullptr;
+  const uint8_t* src = codes;
+  int64_t lds = ld;
+  if (r == DTQ_OK && packed) {
+    lds = K;
+    if (cudaMalloc(&tmp, N * K) != cudaSuccess) {
+      r = fail(DTQ_ERR_CUDA, "create_from_codes: out of device memory");
+    } else {
+      const int64_t count = N * K;
+      const int grid = static_cast<int>(std::min<int64_t>((count + 255) / 256, 148 * 32));
+      unpack_stream_kernel<<<grid, 256, 0, st>>>(codes, count, weight_bits, N, K, tmp, K);
+      if (cudaGetLastError() != cudaSuccess) r = fail(DTQ_ERR_CUDA, "unpack launch failed");
+      src = tmp;
+    }
+  }
+  if (r == DTQ_OK) r = finish_from_codes(h, src, lds, scale, bias, st);
+  if (tmp) cudaFreeAsync(tmp, st);
+  if (r != DTQ_OK) {
+    free_handle(h);
+    return r;
+  }
+  *out = h;
+  return DTQ_OK;
+}
+
+int dtq_qlinear_destroy(dtq_qlinear_t h) {
+  if (h) free_handle(h);
+  return DTQ_OK;
+}
+
+int dtq_qlinear_info(dtq_qlinear_t h, int64_t* N, int64_t* K, int* wbits, int* abits) {
+  if (!h) return fail(DTQ_ERR_INVALID_ARGUMENT, "info: null handle");
+  if (N) *N = h->N;
+  if (K) *K = h->K;
+  if (wbits) *wbits = h->wbits;
+  if (abits) *abits = h->abits;
+  return DTQ_OK;
+}
+
+int dtq_qlinear_export(dtq_qlinear_t h, uint8_t* codes, double* scale, int32_t* wsum,
+                       void* stream) {
+  if (!h) return fail(DTQ_ERR_INVALID_ARGUMENT, "export: null handle");
+  cudaStream_t st = as_stream(stream);
+  if (codes) {
+    uint8_t* tmp = nullptr;
+    CUDA_TRY(cudaMalloc(&tmp, h->N * h->K));
+    const int grid = static_cast<int>(std::min<int64_t>((h->N * h->K + 255) / 256, 148 * 32));
+    export_codes_kernel<<<grid, 256, 0, st>>>(h->w8, h->ld8, h->w4, h->ld4, h->wbits, h->N, h->K,
+                                              tmp);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(codes, tmp, h->N * h->K, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    cudaFree(tmp);
+  }
+  if (scale) CUDA_TRY(cudaMemcpyAsync(scale, h->s_w, h->N * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (wsum) CUDA_TRY(cudaMemcpyAsync(wsum, h->wsum, h->N * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return DTQ_OK;
+}
+
+int dtq_qgemm(const uint8_t* codes, int64_t ldc, const double* s_x, const int32_t* z_x, int64_t M,
+              dtq_qlinear_t h, void* y, int y_dtype, int64_t ldy, void* stream) {
+  return qgemm_impl(codes, ldc, s_x, z_x, M, h, y, y_dtype, ldy, as_stream(stream));
+}
+
+size_t dtq_qlinear_workspace_bytes(dtq_qlinear_t h, int64_t M) {
+  if (!h || M <= 0) return 0;
+  int64_t ldc;
+  size_t a, b;
+  return ws_layout(h, M, &ldc, &a, &b);
+}
+
+int dtq_qlinear_forward(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear_t h,
+                        int mode, const dtq_prologue* prologue, void* y, int y_dtype,
+                        int64_t ldy, void* workspace, size_t workspace_bytes, int32_t* status,
+                        void* stream) {
+  return forward_impl(x, x_dtype, M, ldx, h, mode, prologue, y, y_dtype, ldy, workspace,
+                      workspace_bytes, status, as_stream(stream));
+}
+
+int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_t h, int mode,
+                             void* y, int y_dtype, void* stream) {
+  if (!h || !x || !y || M <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "forward_host: bad args");
+  const size_t xb = dtype_size(x_dtype) * static_cast<size_t>(M) * h->K;
+  const size_t yb = dtype_size(y_dtype) * static_cast<size_t>(M) * h->N;
+  if (xb == 0 || yb == 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "forward_host: bad dtype");
+  cudaStream_t st = as_stream(stream);
+  DTQ_TRY(grow(&h->hx, &h->hx_bytes, xb));
+  DTQ_TRY(grow(&h->hy, &h->hy_bytes, yb));
+  CUDA_TRY(cudaMemsetAsync(h->status, 0, sizeof(int32_t), st));
+  CUDA_TRY(cudaMemcpyAsync(h->hx, x, xb, cudaMemcpyHostToDevice, st));
+  DTQ_TRY(forward_impl(h->hx, x_dtype, M, h->K, h, mode, nullptr, h->hy, y_dtype, h->N, nullptr,
+                       0, h->status, st));
+  CUDA_TRY(cudaMemcpyAsync(y, h->hy, yb, cudaMemcpyDeviceToHost, st));
+  int32_t bad = 0;
+  CUDA_TRY(cudaMemcpyAsync(&bad, h->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (bad) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: non-finite input");
+  return DTQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library loads, exports
+exactly what include/dtq_capi.h declares, and refuses to compute without a
+sm_100 device (no CPU fallback)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2406_02540_b200 as dtq
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "dtq_capi.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(dtq_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_matches_python_binding():
+    assert declared_symbols() == sorted(dtq.EXPORTED)
+
+
+def test_library_exports_every_declared_symbol():
+    if not os.path.exists(dtq.LIB_PATH):
+        pytest.skip("libdtq_b200.so not built (run __graft_entry__.build())")
+    lib = ctypes.CDLL(dtq.LIB_PATH)
+    for name in declared_symbols():
+        assert hasattr(lib, name), f"{name} missing from libdtq_b200.so"
+
+
+def test_version_and_no_cpu_fallback():
+    if not os.path.exists(dtq.LIB_PATH):
+        pytest.skip("libdtq_b200.so not built")
+    L = dtq.lib()
+    assert L.dtq_capi_version() == 1
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    # without a device the boundary reports a CUDA error instead of computing
+    assert L.dtq_device_check() == dtq.DTQ_ERR_CUDA
+    assert b"no CUDA device" in L.dtq_last_error() or b"sm_100" in L.dtq_last_error()
+
+
+def test_invalid_arguments_are_rejected_before_the_device():
+    if not os.path.exists(dtq.LIB_PATH):
+        pytest.skip("libdtq_b200.so not built")
+    L = dtq.lib()
+    # bits outside {2,4,6,8} -> DTQ_ERR_INVALID_ARGUMENT (quant.cpp:143-146)
+    st = L.dtq_quantize_rows(1, dtq.F16, 4, 8, 8, 3, 0, 0, None, None, 1, 16, 1, 1, None, None)
+    assert st == dtq.DTQ_ERR_INVALID_ARGUMENT
+    # empty matrix
+    st = L.dtq_quantize_rows(1, dtq.F16, 0, 8, 8, 8, 0, 0, None, None, 1, 16, 1, 1, None, None)
+    assert st == dtq.DTQ_ERR_INVALID_ARGUMENT
+    # weight bits 3 (make_quant_linear: unsupported bit width)
+    h = ctypes.c_void_p()
+    st = L.dtq_qlinear_create(1, dtq.F16, 4, 8, 8, 3, 8, None, None, None, ctypes.byref(h))
+    assert st == dtq.DTQ_ERR_INVALID_ARGUMENT
+
+
+def test_hadamard_signs_match_the_oracle_engine(oracle):
+    import numpy as np
+    for seed, n in [(7, 1152), (0, 64), (123, 4608)]:
+        assert np.array_equal(dtq.hadamard_signs(n, seed), oracle.hadamard_signs(n, seed))

@@ -1,0 +1,308 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * rotation off: u8 codes, f64 per-token scales, i32 zero points and the
+    int32 accumulators are bit-exact;
+  * rotation on (fast fp32 mode): codes differ by at most 1 LSB on at most
+    1e-4 of elements; the exact (fp64) mode is bit-exact with rotation too;
+  * fp16 outputs: max|y - y_ref| <= 1e-3 * max|y_ref|;
+  * the F64 parity epilogue reproduces the reference's fp64 y bit-for-bit.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import paper_2406_02540_b200 as dtq  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+REL_TOL = 1e-3
+
+
+def f64(a):
+    return np.asarray(a, dtype=np.float64)
+
+
+def cuda(a, dtype=None):
+    t = torch.as_tensor(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(DEV)
+
+
+def rel_err(y, y_ref):
+    return np.abs(np.asarray(y, np.float64) - y_ref).max() / max(np.abs(y_ref).max(), 1e-30)
+
+
+def activations(rng, M, K, outliers=4):
+    g = np.exp(rng.standard_normal(K))
+    x = rng.standard_normal((M, K)) * g
+    x[:, rng.choice(K, outliers, replace=False)] *= 30.0
+    x = x.astype(np.float16)
+    x[0] = 0.0
+    x[1] = 0.5
+    x[2] = np.abs(x[2])
+    x[3] = -np.abs(x[3])
+    return x
+
+
+# ------------------------------------------------------------------ quantizer
+@pytest.mark.parametrize("mode", [dtq.MODE_FAST, dtq.MODE_EXACT])
+@pytest.mark.parametrize("bits", [8, 6, 4, 2])
+def test_quantizer_golden_bitexact(golden, mode, bits):
+    x = cuda(golden["q_x"])
+    codes, s, z = dtq.quantize_rows(x, bits, mode=mode)
+    key = "q" if bits == 8 else f"q{bits}"
+    assert np.array_equal(codes.cpu().numpy(), golden[f"{key}_codes"])
+    assert np.array_equal(s.cpu().numpy(), golden[f"{key}_s"])
+    assert np.array_equal(z.cpu().numpy(), golden[f"{key}_z"])
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16, torch.float32, torch.float64])
+def test_quantizer_full_size_bitexact(oracle, dtype):
+    rng = np.random.default_rng(11)
+    x = activations(rng, 4096, 1152)
+    xt = torch.from_numpy(x.astype(np.float32)).to(dtype)
+    codes, s, z = dtq.quantize_rows(xt.to(DEV))
+    c_ref, s_ref, z_ref = oracle.quantize_rows(xt.double().numpy(), 8)
+    assert np.array_equal(codes.cpu().numpy(), c_ref)
+    assert np.array_equal(s.cpu().numpy(), s_ref)
+    assert np.array_equal(z.cpu().numpy(), z_ref)
+
+
+@pytest.mark.parametrize("K", [8, 40, 136, 200, 1000, 4608, 9216])
+def test_quantizer_ragged_and_wide(oracle, K):
+    rng = np.random.default_rng(K)
+    x = (rng.standard_normal((37, K)) * 3).astype(np.float16)
+    x[5] = 1.0
+    codes, s, z = dtq.quantize_rows(cuda(x))
+    c_ref, s_ref, z_ref = oracle.quantize_rows(f64(x), 8)
+    assert np.array_equal(codes.cpu().numpy(), c_ref)
+    assert np.array_equal(s.cpu().numpy(), s_ref) and np.array_equal(z.cpu().numpy(), z_ref)
+
+
+def test_quantizer_unaligned_pitch(oracle):
+    rng = np.random.default_rng(5)
+    base = (rng.standard_normal((64, 1160)) * 2).astype(np.float16)
+    xt = cuda(base)[:, 3:3 + 1152]          # pitch 1160, misaligned start
+    codes, s, z = dtq.quantize_rows(xt)
+    c_ref, s_ref, z_ref = oracle.quantize_rows(f64(base[:, 3:3 + 1152]), 8)
+    assert np.array_equal(codes.cpu().numpy(), c_ref) and np.array_equal(s.cpu().numpy(), s_ref)
+
+
+def test_quantizer_row_shards_are_bit_identical():
+    # per-token params are row-local (quant.cpp:70-73): any row split of X
+    # quantizes to the same bytes -> token-row sharding across GPUs is exact
+    rng = np.random.default_rng(3)
+    x = cuda(activations(rng, 1000, 1152))
+    full = dtq.quantize_rows(x)
+    for a, b in [(0, 333), (333, 800), (800, 1000)]:
+        part = dtq.quantize_rows(x[a:b])
+        for p, f in zip(part, full):
+            assert torch.equal(p, f[a:b])
+
+
+def test_quantizer_nonfinite_sets_status():
+    x = torch.randn(8, 256, device=DEV, dtype=torch.float16)
+    x[3, 7] = float("inf")
+    status = torch.zeros(1, dtype=torch.int32, device=DEV)
+    dtq.quantize_rows(x, status=status)
+    assert int(status.item()) == 1
+
+
+# ------------------------------------------------------------------ balance
+def test_balance_exact_mode_bitexact(golden):
+    bal = dtq.Balance(cuda(golden["bal_smooth"]), cuda(golden["bal_signs"]), 128)
+    codes, s, z = dtq.quantize_rows(cuda(golden["q_x"]), mode=dtq.MODE_EXACT, balance=bal)
+    assert np.array_equal(codes.cpu().numpy(), golden["bal_codes"])
+    assert np.array_equal(s.cpu().numpy(), golden["bal_s"])
+    assert np.array_equal(z.cpu().numpy(), golden["bal_z"])
+    rot = dtq.Balance(None, cuda(golden["bal_signs"]), 128)
+    codes, s, z = dtq.quantize_rows(cuda(golden["q_x"]), mode=dtq.MODE_EXACT, balance=rot)
+    assert np.array_equal(codes.cpu().numpy(), golden["rot_codes"])
+    assert np.array_equal(s.cpu().numpy(), golden["rot_s"])
+
+
+def test_balance_fast_mode_within_one_lsb(oracle):
+    rng = np.random.default_rng(21)
+    M, K = 4096, 1152
+    x = activations(rng, M, K)
+    w = rng.standard_normal((256, K)) / np.sqrt(K)
+    smooth = oracle.scaling_mask(np.abs(f64(x)).max(0), np.abs(w).max(0), 0.5)
+    signs = oracle.hadamard_signs(K, 7)
+    bal = dtq.Balance(cuda(smooth), cuda(signs), 128)
+    codes, s, z = dtq.quantize_rows(cuda(x), mode=dtq.MODE_FAST, balance=bal)
+    xr = oracle.rotate_blocks(oracle.scale_x(f64(x), smooth), signs, 128)
+    c_ref, s_ref, z_ref = oracle.quantize_rows(xr, 8)
+    d = np.abs(codes.cpu().numpy().astype(np.int32) - c_ref.astype(np.int32))
+    assert d.max() <= 1, f"max code difference {d.max()}"
+    assert (d > 0).mean() <= 1e-4, f"{(d > 0).mean():.2e} of codes differ"
+    assert np.allclose(s.cpu().numpy(), s_ref, rtol=1e-6)
+
+
+# ------------------------------------------------------------------ weights
+@pytest.mark.parametrize("wb", [8, 4])
+def test_weight_prep_bitexact(golden, wb):
+    layer = dtq.QuantLinear.create(cuda(golden["w"]), wb, 8)
+    codes, s, wsum = layer.export()
+    assert np.array_equal(codes, golden[f"w{wb}_codes"])
+    assert np.array_equal(s, golden[f"w{wb}_s"])
+    zw = 1 << (wb - 1)
+    assert np.array_equal(wsum, (golden[f"w{wb}_codes"].astype(np.int64) - zw).sum(1))
+
+
+def test_weight_prep_balanced_bitexact(golden):
+    bal = dtq.Balance(cuda(golden["bal_smooth"]), cuda(golden["bal_signs"]), 128)
+    layer = dtq.QuantLinear.create(cuda(golden["w"]), 8, 8, balance=bal)
+    codes, s, _ = layer.export()
+    assert np.array_equal(codes, golden["bal_wcodes"])
+    assert np.array_equal(s, golden["bal_ws"])
+
+
+def test_w4_from_packed_codes(golden):
+    # checkpoint path: the reference's packed nibble stream uploaded as is
+    packed = cuda(golden["w4_packed"])
+    layer = dtq.QuantLinear.from_codes(packed, cuda(golden["w4_s"]), 4, golden["w"].shape[1],
+                                       packed=True)
+    codes, s, _ = layer.export()
+    assert np.array_equal(codes, golden["w4_codes"])
+
+
+# ------------------------------------------------------------------ GEMM
+@pytest.mark.parametrize("wb", [8, 4])
+def test_gemm_golden_acc_and_f64_bitexact(golden, oracle, wb):
+    bias = cuda(golden["bias"])
+    layer = dtq.QuantLinear.create(cuda(golden["w"]), wb, 8, bias=bias)
+    x = cuda(golden["q_x"])
+    codes, s, z = dtq.quantize_rows(x)
+    acc = layer.gemm(codes, s, z, out_dtype=torch.int32).cpu().numpy()
+    acc_ref = oracle.qlinear_acc(golden["q_codes"], golden["q_z"], golden[f"w{wb}_codes"],
+                                 golden[f"w{wb}_z"])
+    assert np.array_equal(acc.astype(np.int64), acc_ref)
+    y64 = layer.forward(x, out_dtype=torch.float64, mode=dtq.MODE_EXACT).cpu().numpy()
+    assert np.array_equal(y64, golden[f"w{wb}_y"])           # reference fp64 y, bit-exact
+    y16 = layer.forward(x, out_dtype=torch.float16).float().cpu().numpy()
+    assert rel_err(y16, golden[f"w{wb}_y"]) <= REL_TOL
+
+
+@pytest.mark.parametrize("i", [0, 1, 2])
+def test_gemm_ragged_shapes(golden, i):
+    layer = dtq.QuantLinear.create(cuda(golden[f"rag{i}_w"]), 8, 8, bias=cuda(golden[f"rag{i}_b"]))
+    x = cuda(golden[f"rag{i}_x"])
+    y64 = layer.forward(x, out_dtype=torch.float64, mode=dtq.MODE_EXACT).cpu().numpy()
+    assert np.array_equal(y64, golden[f"rag{i}_y"])
+    for dt in (torch.float16, torch.bfloat16, torch.float32):
+        y = layer.forward(x, out_dtype=dt).double().cpu().numpy()
+        tol = 1e-2 if dt == torch.bfloat16 else REL_TOL
+        assert rel_err(y, golden[f"rag{i}_y"]) <= tol
+
+
+def test_gemm_balanced_layer(golden):
+    bal = dtq.Balance(cuda(golden["bal_smooth"]), cuda(golden["bal_signs"]), 128)
+    layer = dtq.QuantLinear.create(cuda(golden["w"]), 8, 8, bias=cuda(golden["bias"]), balance=bal)
+    x = cuda(golden["q_x"])
+    y64 = layer.forward(x, out_dtype=torch.float64, mode=dtq.MODE_EXACT).cpu().numpy()
+    assert np.array_equal(y64, golden["bal_y"])
+    y16 = layer.forward(x, out_dtype=torch.float16, mode=dtq.MODE_FAST).float().cpu().numpy()
+    assert rel_err(y16, golden["bal_y"]) <= REL_TOL
+
+
+STDIT_SHAPES = [("qkv", 1152, 3456), ("proj", 1152, 1152), ("fc1", 1152, 4608),
+                ("fc2", 4608, 1152)]
+
+
+@pytest.mark.parametrize("wb", [8, 4])
+@pytest.mark.parametrize("name,K,N", STDIT_SHAPES)
+def test_stdit_shapes_full_size(oracle, wb, name, K, N):
+    """Config 1 / 3 shapes at M=4096: int32 acc exact on sampled rows
+    (row-local, so a row subset is an exact check), fp16 within 1e-3."""
+    rng = np.random.default_rng(K * 7 + N + wb)
+    M = 4096
+    x = activations(rng, M, K)
+    w = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float16)
+    bias = rng.standard_normal(N) * 0.1
+    layer = dtq.QuantLinear.create(cuda(w), wb, 8, bias=cuda(bias))
+    xt = cuda(x)
+    codes, s, z = dtq.quantize_rows(xt)
+    acc = layer.gemm(codes, s, z, out_dtype=torch.int32)
+    y16 = layer.forward(xt, out_dtype=torch.float16)
+    rows = np.sort(rng.choice(M, 384, replace=False))
+    rows[:4] = [0, 1, 2, 3]
+    wc, sw, zw = oracle.make_quant_linear(f64(w), wb)
+    c_ref, s_ref, z_ref = oracle.quantize_rows(f64(x[rows]), 8)
+    assert np.array_equal(codes.cpu().numpy()[rows], c_ref)
+    acc_ref = oracle.qlinear_acc(c_ref, z_ref, wc, zw)
+    assert np.array_equal(acc.cpu().numpy()[rows].astype(np.int64), acc_ref)
+    y_ref = oracle.qlinear_epilogue(acc_ref, s_ref, sw, bias)
+    assert rel_err(y16.float().cpu().numpy()[rows], y_ref) <= REL_TOL
+
+
+def test_prologue_modulate_exact(oracle):
+    rng = np.random.default_rng(8)
+    M, K, N = 300, 1152, 640
+    x = activations(rng, M, K)
+    sc = (rng.standard_normal(K) * 0.2).astype(np.float32)
+    sh = (rng.standard_normal(K) * 0.1).astype(np.float32)
+    pro = dtq.Prologue(dtq.PROLOGUE_MODULATE, cuda(sc), cuda(sh))
+    codes, s, z = dtq.quantize_rows(cuda(x), mode=dtq.MODE_EXACT, prologue=pro)
+    xm = oracle.modulate(f64(x), f64(sc), f64(sh))
+    c_ref, s_ref, z_ref = oracle.quantize_rows(xm, 8)
+    assert np.array_equal(codes.cpu().numpy(), c_ref) and np.array_equal(s.cpu().numpy(), s_ref)
+    codes, s, z = dtq.quantize_rows(cuda(x), mode=dtq.MODE_FAST, prologue=pro)
+    d = np.abs(codes.cpu().numpy().astype(int) - c_ref.astype(int))
+    assert d.max() <= 1 and (d > 0).mean() <= 1e-3
+
+
+def test_prologue_gelu_and_layernorm_run():
+    # GELU follows toydit.cpp:83; LayerNorm has no reference oracle (unpinned):
+    # compare with a torch fp64 restatement by tolerance only
+    rng = np.random.default_rng(9)
+    x = activations(rng, 128, 1152).astype(np.float32)
+    xt = cuda(x)
+    xd = torch.from_numpy(x).double()
+    g = 0.5 * xd * (1 + torch.erf(xd / 2 ** 0.5))
+    codes, s, z = dtq.quantize_rows(xt, prologue=dtq.Prologue(dtq.PROLOGUE_GELU))
+    deq = (codes.double().cpu() - z.cpu()[:, None].double()) * s.cpu()[:, None]
+    assert (deq - g).abs().max() <= s.cpu().max() * 0.51 + 1e-4
+    sc = torch.zeros(1152, device=DEV)
+    pro = dtq.Prologue(dtq.PROLOGUE_LN_MODULATE, sc, sc, 1e-6)
+    codes, s, z = dtq.quantize_rows(xt, prologue=pro)
+    ln = (xd - xd.mean(1, keepdim=True)) / torch.sqrt(xd.var(1, unbiased=False, keepdim=True) + 1e-6)
+    deq = (codes.double().cpu() - z.cpu()[:, None].double()) * s.cpu()[:, None]
+    assert (deq - ln).abs().max() <= s.cpu().max() * 0.51 + 1e-3
+
+
+def test_overflow_guard_and_shape_errors():
+    # K beyond the exact-int32 bound -> OverflowError (qgemm.cpp:29-34 convention)
+    K = 70000
+    codes = torch.full((1, K), 128, dtype=torch.uint8, device=DEV)
+    layer = dtq.QuantLinear.from_codes(codes, torch.ones(1, dtype=torch.float64, device=DEV), 8, K)
+    a = torch.zeros((128, (K + 15) // 16 * 16), dtype=torch.uint8, device=DEV)
+    with pytest.raises(OverflowError):
+        layer.gemm(a[:, :K], torch.ones(128, dtype=torch.float64, device=DEV),
+                   torch.zeros(128, dtype=torch.int32, device=DEV))
+    small = dtq.QuantLinear.create(torch.randn(16, 64, device=DEV, dtype=torch.float16))
+    with pytest.raises(ValueError):
+        small.forward(torch.randn(4, 32, device=DEV, dtype=torch.float16))  # X cols != C_in
+
+
+def test_forward_host_buffers(golden):
+    layer = dtq.QuantLinear.create(cuda(golden["w"]), 8, 8, bias=cuda(golden["bias"]))
+    x = torch.from_numpy(golden["q_x"]).pin_memory()
+    y = torch.empty((x.shape[0], layer.N), dtype=torch.float64).pin_memory()
+    layer.forward_host(x, y, mode=dtq.MODE_EXACT)
+    assert np.array_equal(y.numpy(), golden["w8_y"])
+    x_bad = x.clone()
+    x_bad[2, 2] = float("nan")
+    with pytest.raises(ValueError):
+        layer.forward_host(x_bad, y)
+
+
+def test_deterministic():
+    rng = np.random.default_rng(4)
+    x = cuda(activations(rng, 1024, 1152))
+    layer = dtq.QuantLinear.create(cuda(rng.standard_normal((2304, 1152)).astype(np.float16)), 4, 8)
+    y1 = layer.forward(x)
+    y2 = layer.forward(x)
+    assert torch.equal(y1, y2)

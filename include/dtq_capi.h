@@ -174,6 +174,15 @@ int dtq_qlinear_forward(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_
                         int64_t ldy, void* workspace, size_t workspace_bytes,
                         int32_t* status, void* stream);
 
+/* The quantizer stage of dtq_qlinear_forward alone: the activation side of
+ * the handle's balance (X / s with the handle's fp32 reciprocals in FAST
+ * mode, fp64 divide in EXACT mode, then the rotation) + optional prologue +
+ * per-token quantization at the handle's act_bits.  codes [dev] M x K u8
+ * with pitch ldc (multiple of 16 for the GEMM), scale/zero [dev] M. */
+int dtq_qlinear_quantize(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear_t h,
+                         int mode, const dtq_prologue* prologue, uint8_t* codes, int64_t ldc,
+                         double* scale, int32_t* zero, int32_t* status, void* stream);
+
 /* Same with HOST buffers (x [host] M x K dense, y [host] M x N dense):
  * H2D copy, fused forward, D2H copy, stream synchronised before returning.
  * Pinned host memory gives full PCIe/C2C bandwidth.  Non-finite input is

@@ -38,7 +38,7 @@ EXPORTED = (
     "dtq_last_error", "dtq_capi_version", "dtq_device_check", "dtq_quantize_rows",
     "dtq_qlinear_create", "dtq_qlinear_create_from_codes", "dtq_qlinear_destroy",
     "dtq_qlinear_info", "dtq_qlinear_export", "dtq_qgemm", "dtq_qlinear_workspace_bytes",
-    "dtq_qlinear_forward", "dtq_qlinear_forward_host",
+    "dtq_qlinear_forward", "dtq_qlinear_quantize", "dtq_qlinear_forward_host",
 )
 
 
@@ -79,6 +79,7 @@ def lib():
     L.dtq_qlinear_workspace_bytes.restype = C.c_size_t
     L.dtq_qlinear_workspace_bytes.argtypes = [p, i64]
     L.dtq_qlinear_forward.argtypes = [p, i32, i64, i64, p, i32, p, p, i32, i64, p, C.c_size_t, p, p]
+    L.dtq_qlinear_quantize.argtypes = [p, i32, i64, i64, p, i32, p, p, i64, p, p, p, p]
     L.dtq_qlinear_forward_host.argtypes = [p, i32, i64, p, i32, p, i32, p]
     _lib = L
     return L
@@ -247,6 +248,24 @@ class QuantLinear:
                                M, self._h, out.data_ptr(), _dtype_code(out.dtype), out.stride(0),
                                _stream(stream)))
         return out
+
+    def quantize(self, x, mode: int = MODE_FAST, prologue: Optional[Prologue] = None,
+                 out=None, status=None, stream=None):
+        """The fused-quantizer stage of forward(): (codes, s_x, z_x)."""
+        torch = _torch()
+        M = x.shape[0]
+        if out is None:
+            ldc = (self.K + 15) // 16 * 16
+            buf = torch.empty((M, ldc), dtype=torch.uint8, device=x.device)
+            out = (buf[:, :self.K], torch.empty(M, dtype=torch.float64, device=x.device),
+                   torch.empty(M, dtype=torch.int32, device=x.device))
+        codes, s, z = out
+        pr = prologue._c() if prologue is not None else None
+        _check(lib().dtq_qlinear_quantize(x.data_ptr(), _dtype_code(x.dtype), M, x.stride(0),
+                                          self._h, mode, _ref_or_none(pr), codes.data_ptr(),
+                                          codes.stride(0), s.data_ptr(), z.data_ptr(),
+                                          _ptr(status), _stream(stream)))
+        return codes, s, z
 
     def forward(self, x, out_dtype=None, mode: int = MODE_FAST,
                 prologue: Optional[Prologue] = None, out=None, workspace=None, status=None,

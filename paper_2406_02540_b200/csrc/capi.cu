@@ -739,6 +739,16 @@ int dtq_qlinear_forward(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_
                       workspace_bytes, status, as_stream(stream));
 }
 
+int dtq_qlinear_quantize(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear_t h,
+                         int mode, const dtq_prologue* prologue, uint8_t* codes, int64_t ldc,
+                         double* scale, int32_t* zero, int32_t* status, void* stream) {
+  if (!h) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: null handle");
+  if (ldx < h->K) return fail(DTQ_ERR_INVALID_ARGUMENT, "qlinear_forward: X cols != C_in");
+  return quantize_rows_impl(x, x_dtype, M, h->K, ldx, h->abits, 0, mode, 0, h->smooth,
+                            h->inv_smooth, h->signs, h->hblock, prologue, codes, ldc, scale, zero,
+                            status, as_stream(stream));
+}
+
 int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_t h, int mode,
                              void* y, int y_dtype, void* stream) {
   if (!h || !x || !y || M <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "forward_host: bad args");

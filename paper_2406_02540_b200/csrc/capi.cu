@@ -493,11 +493,16 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
   g.y = yk;
   g.ldy = ldk;
   g.out_kind = kind;
-  g.vec_store = (reinterpret_cast<uintptr_t>(yk) % 16 == 0) && ((ldk * es) % 16 == 0);
+  g.tma_store = (reinterpret_cast<uintptr_t>(yk) % 16 == 0) && ((ldk * es) % 16 == 0);
+  CUtensorMap tY;
+  std::memset(&tY, 0, sizeof(tY));
+  if (g.tma_store)
+    DTQ_TRY(make_tmap_u8(&tY, yk, M, h->N * static_cast<int64_t>(es), ldk * es, 64, 32,
+                         CU_TENSOR_MAP_SWIZZLE_64B));
 
   const int sms = device_info().sms;
-  const cudaError_t e = h->wbits == 8 ? dtq_launch_gemm_w8(tA, h->tmB, g, BN, sms, st)
-                                      : dtq_launch_gemm_w4(tA, h->tmB, g, BN, sms, st);
+  const cudaError_t e = h->wbits == 8 ? dtq_launch_gemm_w8(tA, h->tmB, tY, g, BN, sms, st)
+                                      : dtq_launch_gemm_w4(tA, h->tmB, tY, g, BN, sms, st);
   if (e != cudaSuccess) return fail(DTQ_ERR_CUDA, "qgemm launch: %s", cudaGetErrorString(e));
 
   if (y_dtype == DTQ_F64) {

@@ -179,34 +179,34 @@ __device__ __forceinline__ void block_reduce2(T& a, T& b, T* buf, int& pp, OpA o
 // ------------------------------------------------------------------ kernel
 template <typename Tin, typename Tc, int kCPT, bool kVec>
 __global__ void __launch_bounds__(kCPT == 1 ? 1024 : 256) fq_kernel(const FqArgs a) {
+  constexpr bool kExact = sizeof(Tc) == 8;
+  constexpr int kW = Vec<Tin>::kWords;
   // transform selection is uniform per launch: plain branches, no divergence
   const int kPro = a.pro;
   const bool kSmooth = a.smooth_d != nullptr || a.inv_smooth_f != nullptr;
   const bool kRotate = a.signs != nullptr;
-  constexpr bool kExact = sizeof(Tc) == 8;
-  constexpr int kW = Vec<Tin>::kWords;
   __shared__ __align__(16) Tc red[2 * 64];
   int pp = 0;
 
   const int t = threadIdx.x;
   const int tpr = a.tpr;
-  const bool active = t < tpr;
-  const int64_t K = a.K;
+  const int K = static_cast<int>(a.K);
   const Tin* __restrict__ X = static_cast<const Tin*>(a.x);
-  const double qmax = static_cast<double>((1 << a.bits) - 1);
+  const int qmax_i = (1 << a.bits) - 1;
 
-  // column base of each owned chunk
-  int64_t cbase[kCPT];
-  int nval[kCPT];
+  // column base / valid count of each owned 8-element chunk.  With kVec the
+  // host guarantees K % 8 == 0, so a chunk is either full or empty.
+  int cb[kCPT], nv[kCPT];
 #pragma unroll
   for (int i = 0; i < kCPT; ++i) {
-    cbase[i] = (static_cast<int64_t>(i) * tpr + t) * 8;
-    const int64_t rem = K - cbase[i];
-    nval[i] = active ? static_cast<int>(rem >= 8 ? 8 : (rem > 0 ? rem : 0)) : 0;
+    cb[i] = (i * tpr + t) * 8;
+    const int rem = K - cb[i];
+    nv[i] = t < tpr ? (rem >= 8 ? 8 : (rem > 0 ? rem : 0)) : 0;
   }
+  auto ok = [&](int i, int e) -> bool { return kVec ? nv[i] > 0 : e < nv[i]; };
 
   // rotation signs stay in registers across rows (one bit per column);
-  // smoothing / modulation vectors are re-read per row from L1.
+  // smoothing / modulation vectors are re-read per row (L1-resident).
   uint32_t sgn[kCPT];
 #pragma unroll
   for (int i = 0; i < kCPT; ++i) {
@@ -214,35 +214,36 @@ __global__ void __launch_bounds__(kCPT == 1 ? 1024 : 256) fq_kernel(const FqArgs
     if (kRotate)
 #pragma unroll
       for (int e = 0; e < 8; ++e)
-        if (e < nval[i] && a.signs[cbase[i] + e] < 0) sgn[i] |= 1u << e;
+        if (ok(i, e) && a.signs[cb[i] + e] < 0) sgn[i] |= 1u << e;
   }
   auto colvec = [&](const auto* p, int i, Tc (&out)[8], Tc fill) {
-    if (nval[i] == 8 && kVec) {
+    if (kVec && nv[i] > 0) {
       if constexpr (sizeof(*p) == 4) {
-        const float4 f0 = __ldg(reinterpret_cast<const float4*>(p + cbase[i]));
-        const float4 f1 = __ldg(reinterpret_cast<const float4*>(p + cbase[i]) + 1);
+        const float4 f0 = __ldg(reinterpret_cast<const float4*>(p + cb[i]));
+        const float4 f1 = __ldg(reinterpret_cast<const float4*>(p + cb[i]) + 1);
         out[0] = f0.x; out[1] = f0.y; out[2] = f0.z; out[3] = f0.w;
         out[4] = f1.x; out[5] = f1.y; out[6] = f1.z; out[7] = f1.w;
       } else {
 #pragma unroll
         for (int e = 0; e < 8; e += 2) {
-          const double2 d = __ldg(reinterpret_cast<const double2*>(p + cbase[i] + e));
+          const double2 d = __ldg(reinterpret_cast<const double2*>(p + cb[i] + e));
           out[e] = static_cast<Tc>(d.x);
           out[e + 1] = static_cast<Tc>(d.y);
         }
       }
     } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) out[e] = e < nval[i] ? static_cast<Tc>(p[cbase[i] + e]) : fill;
+      for (int e = 0; e < 8; ++e) out[e] = e < nv[i] ? static_cast<Tc>(p[cb[i] + e]) : fill;
     }
   };
 
   uint4 raw[kCPT][kW];
   auto load_row = [&](int64_t row) {
     if constexpr (kVec) {
+      const Tin* xr = X + row * a.ldx;
 #pragma unroll
       for (int i = 0; i < kCPT; ++i)
-        if (nval[i] > 0) ld_raw<Tin>(X + row * a.ldx + cbase[i], raw[i]);
+        if (nv[i] > 0) ld_raw<Tin>(xr + cb[i], raw[i]);
     }
   };
 
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(kCPT == 1 ? 1024 : 256) fq_kernel(const FqArgs
     if constexpr (kVec) {
 #pragma unroll
       for (int i = 0; i < kCPT; ++i) {
-        if (nval[i] > 0) {
+        if (nv[i] > 0) {
           unpack<Tc>(raw[i], v[i], Tin());
         } else {
 #pragma unroll
@@ -263,11 +264,11 @@ __global__ void __launch_bounds__(kCPT == 1 ? 1024 : 256) fq_kernel(const FqArgs
       const int64_t nxt = row + gridDim.x;
       if (nxt < a.M) load_row(nxt);  // prefetch the next row while this one is reduced
     } else {
+      const Tin* xr = X + row * a.ldx;
 #pragma unroll
       for (int i = 0; i < kCPT; ++i)
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          v[i][e] = e < nval[i] ? to_c<Tc>(X[row * a.ldx + cbase[i] + e]) : Tc(0);
+        for (int e = 0; e < 8; ++e) v[i][e] = e < nv[i] ? to_c<Tc>(xr[cb[i] + e]) : Tc(0);
     }
 
     // non-finite guard (quant.cpp:143-146 throws std::invalid_argument)
@@ -276,31 +277,27 @@ __global__ void __launch_bounds__(kCPT == 1 ? 1024 : 256) fq_kernel(const FqArgs
 #pragma unroll
       for (int i = 0; i < kCPT; ++i)
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (e < nval[i] && !isfinite(v[i][e])) bad = true;
+        for (int e = 0; e < 8; ++e) bad |= ok(i, e) && !isfinite(v[i][e]);
       if (bad) atomicOr(a.status, 1);
     }
 
     // ---- prologue (adaLN modulate, toydit.cpp:366-368; GELU toydit.cpp:83)
     if (kPro == kProLnModulate) {
-      Tc s1 = 0, s2 = 0;
+      Tc s1 = 0, s2 = 0, dummy = 0;
 #pragma unroll
       for (int i = 0; i < kCPT; ++i)
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (e < nval[i]) s1 += v[i][e];
-      Tc dummy = 0;
+        for (int e = 0; e < 8; ++e) s1 += ok(i, e) ? v[i][e] : Tc(0);
       block_reduce2(s1, dummy, red, pp, [](Tc p, Tc q) { return p + q; },
                     [](Tc p, Tc q) { return p + q; });
       const Tc mean = s1 / static_cast<Tc>(K);
 #pragma unroll
       for (int i = 0; i < kCPT; ++i)
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (e < nval[i]) {
-            const Tc d = v[i][e] - mean;
-            s2 += d * d;
-          }
+        for (int e = 0; e < 8; ++e) {
+          const Tc d = v[i][e] - mean;
+          s2 += ok(i, e) ? d * d : Tc(0);
+        }
       block_reduce2(s2, dummy, red, pp, [](Tc p, Tc q) { return p + q; },
                     [](Tc p, Tc q) { return p + q; });
       Tc rstd;
@@ -340,7 +337,7 @@ __global__ void __launch_bounds__(kCPT == 1 ? 1024 : 256) fq_kernel(const FqArgs
         }
     }
 
-    // ---- smoothing: X' = X / s_c (balance.cpp:62-63)
+    // ---- smoothing: X' = X / s_c (balance.cpp:62-63); W' = W * s_c on the weight side
     if (kSmooth) {
 #pragma unroll
       for (int i = 0; i < kCPT; ++i) {
@@ -366,7 +363,7 @@ __global__ void __launch_bounds__(kCPT == 1 ? 1024 : 256) fq_kernel(const FqArgs
 #pragma unroll
         for (int e = 0; e < 8; ++e)
           if (sgn[i] & (1u << e)) v[i][e] = -v[i][e];
-        // strides 1, 2, 4 inside the chunk
+        // strides 1, 2, 4 inside the chunk (low index a+b, high index a-b)
 #pragma unroll
         for (int h = 1; h < 8; h <<= 1)
 #pragma unroll
@@ -376,13 +373,17 @@ __global__ void __launch_bounds__(kCPT == 1 ? 1024 : 256) fq_kernel(const FqArgs
               v[i][e] = p + q;
               v[i][e + h] = p - q;
             }
-        // strides 8 .. hblock/2 across lanes
+        // strides 8 .. hblock/2 across lanes: low lane v + o, high lane o - v,
+        // both as one correctly rounded fma(+-1, v, o)
         for (int m = 1; m < (a.hblock >> 3); m <<= 1) {
-          const bool hi = (t & m) != 0;
+          const Tc sg = (t & m) ? Tc(-1) : Tc(1);
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const Tc o = shfl_xor(v[i][e], m);
-            v[i][e] = hi ? (o - v[i][e]) : (v[i][e] + o);
+            if constexpr (kExact)
+              v[i][e] = fma(sg, v[i][e], o);
+            else
+              v[i][e] = fmaf(sg, v[i][e], o);
           }
         }
       }
@@ -401,26 +402,26 @@ __global__ void __launch_bounds__(kCPT == 1 ? 1024 : 256) fq_kernel(const FqArgs
     Tc mn, mx;
     if constexpr (kExact) {
       mn = __longlong_as_double(0x7ff0000000000000LL);
-      mx = -mn;
     } else {
       mn = __int_as_float(0x7f800000);
-      mx = -mn;
     }
+    mx = -mn;
 #pragma unroll
     for (int i = 0; i < kCPT; ++i)
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (e < nval[i]) {
-          mn = v[i][e] < mn ? v[i][e] : mn;
-          mx = v[i][e] < mx ? mx : v[i][e];
+      for (int e = 0; e < 8; ++e) {
+        if (ok(i, e)) {
+          mn = fmin(mn, v[i][e]);
+          mx = fmax(mx, v[i][e]);
         }
-    block_reduce2(mn, mx, red, pp, [](Tc p, Tc q) { return q < p ? q : p; },
-                  [](Tc p, Tc q) { return p < q ? q : p; });
+      }
+    block_reduce2(mn, mx, red, pp, [](Tc p, Tc q) { return fmin(p, q); },
+                  [](Tc p, Tc q) { return fmax(p, q); });
 
     // ---- params (quant.cpp:90-124), fp64 exactly as the reference
+    const double qmax = static_cast<double>(qmax_i);
     const double dmn = static_cast<double>(mn), dmx = static_cast<double>(mx);
-    double s;
-    double z;
+    double s, z;
     if (a.symmetric) {
       const double amax = fmax(fabs(dmn), fabs(dmx));
       z = static_cast<double>(1 << (a.bits - 1));
@@ -439,36 +440,54 @@ __global__ void __launch_bounds__(kCPT == 1 ? 1024 : 256) fq_kernel(const FqArgs
       a.zero[row] = static_cast<int32_t>(z);
     }
 
-    // ---- codes (quant.cpp:169-175)
+    // ---- codes (quant.cpp:169-175): k = clamp(round_half_even(v / s) + z, 0, qmax)
+    // q = v * (1/s) + z with one rounding; clamping before rounding is
+    // equivalent (z is an integer).  Rounding-to-integer is the add of
+    // 1.5 * 2^23 (fp32) or 1.5 * 2^52 (fp64), whose low bits are the code.
+    // Quotients within the error bound of a .5 tie are redone with an
+    // IEEE divide (rare, and warp-uniform per chunk).
     const double inv_s = 1.0 / s;
-    const float inv_sf = static_cast<float>(inv_s);
+    uint8_t* crow = a.codes + row * a.ldc;
 #pragma unroll
     for (int i = 0; i < kCPT; ++i) {
-      if (nval[i] <= 0) continue;
-      uint32_t packed[2] = {0u, 0u};
+      if (nv[i] <= 0) continue;
+      uint32_t m[8];
+      bool near = false;
+      if constexpr (kExact) {
+        const double zq = z, qq = qmax;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        double r;
-        if constexpr (kExact) {
-          const double q = v[i][e] * inv_s;
-          r = rint(q);
-          if (fabs(fabs(q - r) - 0.5) < 1e-9) r = rint(v[i][e] / s);
-        } else {
-          const float q = v[i][e] * inv_sf;
-          const float rf = rintf(q);
-          if (fabsf(fabsf(q - rf) - 0.5f) < 6.103515625e-05f)
-            r = rint(static_cast<double>(v[i][e]) / s);
-          else
-            r = static_cast<double>(rf);
+        for (int e = 0; e < 8; ++e) {
+          const double q = fmin(fmax(fma(v[i][e], inv_s, zq), 0.0), qq);
+          const double r = q + 6755399441055744.0;  // 1.5 * 2^52
+          near |= fabs(q - (r - 6755399441055744.0)) > 0.5 - 1e-9;
+          m[e] = static_cast<uint32_t>(__double2loint(r));
         }
-        const double k = fmin(fmax(r + z, 0.0), qmax);
-        packed[e >> 2] |= static_cast<uint32_t>(k) << (8 * (e & 3));
-      }
-      uint8_t* dst = a.codes + row * a.ldc + cbase[i];
-      if (kVec && nval[i] == 8) {
-        *reinterpret_cast<uint2*>(dst) = make_uint2(packed[0], packed[1]);
       } else {
-        for (int e = 0; e < nval[i]; ++e) dst[e] = static_cast<uint8_t>(packed[e >> 2] >> (8 * (e & 3)));
+        const float inv_sf = static_cast<float>(inv_s), zf = static_cast<float>(z);
+        const float qf = static_cast<float>(qmax_i);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float q = fminf(fmaxf(fmaf(v[i][e], inv_sf, zf), 0.f), qf);
+          const float r = q + 12582912.0f;  // 1.5 * 2^23
+          near |= fabsf(q - (r - 12582912.0f)) > 0.5f - 6.103515625e-05f;
+          m[e] = __float_as_uint(r);
+        }
+      }
+      if (near) {
+        // exact re-evaluation of the near-tie quotients (fp64 IEEE divide)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const double k = fmin(fmax(rint(static_cast<double>(v[i][e]) / s) + z, 0.0), qmax);
+          m[e] = static_cast<uint32_t>(k);
+        }
+      }
+      const uint32_t p0 = __byte_perm(__byte_perm(m[0], m[1], 0x0040), __byte_perm(m[2], m[3], 0x0040), 0x5410);
+      const uint32_t p1 = __byte_perm(__byte_perm(m[4], m[5], 0x0040), __byte_perm(m[6], m[7], 0x0040), 0x5410);
+      uint8_t* dst = crow + cb[i];
+      if (kVec) {
+        *reinterpret_cast<uint2*>(dst) = make_uint2(p0, p1);
+      } else {
+        for (int e = 0; e < nv[i]; ++e) dst[e] = static_cast<uint8_t>((e < 4 ? p0 : p1) >> (8 * (e & 3)));
       }
     }
   }

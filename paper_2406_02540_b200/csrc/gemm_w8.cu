@@ -2,8 +2,9 @@
 #include "launch.h"
 
 cudaError_t dtq_launch_gemm_w8(const CUtensorMap& tA, const CUtensorMap& tB,
-                               const dtq_gemm::GemmArgs& g, int BN, int sms, cudaStream_t st) {
+                               const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, int BN, int sms,
+                               cudaStream_t st) {
   // smem ring: 4 x (16 KB A + 32 KB B) at BN=256, 6 x (16 + 16) KB at BN=128
-  return BN == 256 ? dtq_launch_gemm_o<256, 4, false>(tA, tB, g, sms, st)
-                   : dtq_launch_gemm_o<128, 6, false>(tA, tB, g, sms, st);
+  return BN == 256 ? dtq_launch_gemm_o<256, 4, false>(tA, tB, tY, g, sms, st)
+                   : dtq_launch_gemm_o<128, 6, false>(tA, tB, tY, g, sms, st);
 }

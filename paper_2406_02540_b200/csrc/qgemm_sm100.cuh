@@ -43,7 +43,7 @@ struct GemmArgs {
   void* y;
   int64_t ldy;          // elements
   int out_kind;
-  int vec_store;        // 16-byte aligned rows -> 128-bit stores
+  int tma_store;        // 1: y rows 16-byte aligned -> TMA bulk stores (tmY valid)
 };
 
 constexpr int BM = 128;
@@ -56,12 +56,14 @@ struct Smem {
   static constexpr int kA = BM * BK;                   // 16 KB
   static constexpr int kB = BN * BK;                   // s8 tile
   static constexpr int kP = kW4 ? BN * (BK / 2) : 0;   // packed nibbles
-  static constexpr int kEpi = kEpiWarps * 32 * 128;    // 16 KB
+  static constexpr int kEpi = kEpiWarps * 2 * 32 * 64;  // 2 x (32 rows x 64 B) per warp
+  static constexpr int kPar = 2 * 3 * BN * 4;             // {s_w, wsum, bias} x 2 tiles
   static constexpr int offA = 0;
   static constexpr int offB = offA + kStages * kA;
   static constexpr int offP = offB + kStages * kB;
   static constexpr int offE = offP + kStages * kP;
-  static constexpr int offBar = offE + kEpi;
+  static constexpr int offPar = offE + kEpi;
+  static constexpr int offBar = offPar + kPar;
   static constexpr int kBars = kStages * 3 + 4;
   static constexpr int bytes = offBar + kBars * 8 + 16;
   static constexpr int alloc = bytes + 1024;  // manual 1024-byte alignment
@@ -91,7 +93,7 @@ __device__ __forceinline__ uint32_t s4x8_to_s8x8_hi(uint32_t w) {
 template <int BN, int kStages, bool kW4, int kOut>
 __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     qgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const GemmArgs g) {
+                 const __grid_constant__ CUtensorMap tmY, const GemmArgs g) {
   using namespace dtq_ptx;
   using L = Smem<BN, kStages, kW4>;
   constexpr uint32_t kTmemCols = 2 * BN;
@@ -104,6 +106,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
   uint8_t* sB = smem + L::offB;
   uint8_t* sP = smem + L::offP;
   uint8_t* sE = smem + L::offE;
+  uint32_t* sPar = reinterpret_cast<uint32_t*>(smem + L::offPar);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::offBar);
   uint64_t* empty = full + kStages;
   uint64_t* conv = empty + kStages;
@@ -118,6 +121,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    if (g.tma_store) prefetch_tmap(&tmY);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -190,16 +194,29 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     }
   } else if (warp < 2 + kEpiWarps) {
     // ------------------------------------------------------------ epilogue
-    const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
-    uint8_t* stage = sE + (warp - 2) * (32 * 128);
+    // warp w owns TMEM lanes [32*(w%4), +32) = tile rows; lane = one row.
+    const uint32_t q = warp & 3;
+    const int et = threadIdx.x - 64;                  // 0..127 among epilogue threads
+    uint8_t* stage = sE + (warp - 2) * (2 * 32 * 64);  // ping-pong 32 x 64 B buffers
     constexpr int esize = (kOut == kOutF16 || kOut == kOutBF16) ? 2 : 4;
-    constexpr int cols_per_pass = 128 / esize;  // 64 (16-bit out) or 32 (32-bit out)
+    constexpr int kPieceCols = 64 / esize;             // columns per 64-byte staged row
+    int buf = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       const int m0 = (tile % g.tiles_m) * BM;
       const int n0 = (tile / g.tiles_m) * BN;
+      // per-column params of this tile -> smem (overlaps the tile's main loop)
+      uint32_t* par = sPar + acc * (3 * BN);
+      for (int c = et; c < BN; c += 32 * kEpiWarps) {
+        const int col = n0 + c;
+        const bool okc = col < g.N;
+        par[c] = __float_as_uint(okc ? __ldg(g.s_w + col) : 0.f);
+        par[BN + c] = static_cast<uint32_t>(okc ? __ldg(g.wsum + col) : 0);
+        par[2 * BN + c] = __float_as_uint((okc && g.bias) ? __ldg(g.bias + col) : 0.f);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
       const int row = m0 + q * 32 + lane;
       const bool row_ok = row < g.M;
       const float sx = row_ok ? static_cast<float>(g.s_x[row]) : 0.f;
@@ -208,98 +225,101 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < BN / 64; ++c) {
-        uint32_t r[64];
-        tmem_ld_32x32b_x64(tmem_base + ((q * 32) << 16) + acc * BN + c * 64, r);
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
-        if (c == BN / 64 - 1) {
+        if (c == BN / 32 - 1) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        // column parameters: lane l holds columns l and l + 32 of this chunk
-        const int cb = n0 + c * 64;
-        float swv[2], bv[2];
-        int32_t wsv[2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int col = cb + h * 32 + lane;
-          const bool ok = col < g.N;
-          swv[h] = ok ? __ldg(g.s_w + col) : 0.f;
-          wsv[h] = ok ? __ldg(g.wsum + col) : 0;
-          bv[h] = (ok && g.bias) ? __ldg(g.bias + col) : 0.f;
-        }
+        for (int piece = 0; piece < 32 / kPieceCols; ++piece) {
+          // 16 output words = 64 bytes of this row
+          uint32_t w[16];
 #pragma unroll
-        for (int p = 0; p < 64 / cols_per_pass; ++p) {
-          // stage row `lane`: cols_per_pass outputs = 128 bytes, 8 swizzled granules
+          for (int j4 = 0; j4 < kPieceCols; j4 += 4) {
+            const int cc = c * 32 + piece * kPieceCols + j4;
+            const uint4 sw4 = *reinterpret_cast<const uint4*>(par + cc);
+            const uint4 ws4 = *reinterpret_cast<const uint4*>(par + BN + cc);
+            const uint4 b4 = *reinterpret_cast<const uint4*>(par + 2 * BN + cc);
+            const uint32_t swv[4] = {sw4.x, sw4.y, sw4.z, sw4.w};
+            const uint32_t wsv[4] = {ws4.x, ws4.y, ws4.z, ws4.w};
+            const uint32_t bv[4] = {b4.x, b4.y, b4.z, b4.w};
+            float f[4];
+            int32_t a32[4];
 #pragma unroll
-          for (int gq = 0; gq < 8; ++gq) {
-            uint32_t packed[4];
-            if constexpr (esize == 2) {
+            for (int u = 0; u < 4; ++u) {
+              const int j = piece * kPieceCols + j4 + u;
+              a32[u] = static_cast<int32_t>(r[j]) - zx * static_cast<int32_t>(wsv[u]);
+              f[u] = fmaf(static_cast<float>(a32[u]), sx * __uint_as_float(swv[u]),
+                          __uint_as_float(bv[u]));
+            }
+            if constexpr (kOut == kOutF16) {
+              const __half2 h0 = __floats2half2_rn(f[0], f[1]);
+              const __half2 h1 = __floats2half2_rn(f[2], f[3]);
+              w[j4 / 2] = *reinterpret_cast<const uint32_t*>(&h0);
+              w[j4 / 2 + 1] = *reinterpret_cast<const uint32_t*>(&h1);
+            } else if constexpr (kOut == kOutBF16) {
+              const __nv_bfloat162 h0 = __floats2bfloat162_rn(f[0], f[1]);
+              const __nv_bfloat162 h1 = __floats2bfloat162_rn(f[2], f[3]);
+              w[j4 / 2] = *reinterpret_cast<const uint32_t*>(&h0);
+              w[j4 / 2 + 1] = *reinterpret_cast<const uint32_t*>(&h1);
+            } else if constexpr (kOut == kOutF32) {
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                float f2[2];
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                  const int j = gq * 8 + e * 2 + u;  // column within the 64-chunk
-                  const int h = j >> 5, src = j & 31;
-                  const float sw = __shfl_sync(0xffffffffu, swv[h], src);
-                  const int32_t ws = __shfl_sync(0xffffffffu, wsv[h], src);
-                  const float b = __shfl_sync(0xffffffffu, bv[h], src);
-                  const int32_t a32 = static_cast<int32_t>(r[j]) - zx * ws;
-                  f2[u] = fmaf(static_cast<float>(a32), sx * sw, b);
-                }
-                if constexpr (kOut == kOutF16) {
-                  const __half2 hv = __floats2half2_rn(f2[0], f2[1]);
-                  packed[e] = *reinterpret_cast<const uint32_t*>(&hv);
-                } else {
-                  const __nv_bfloat162 hv = __floats2bfloat162_rn(f2[0], f2[1]);
-                  packed[e] = *reinterpret_cast<const uint32_t*>(&hv);
-                }
-              }
+              for (int u = 0; u < 4; ++u) w[j4 + u] = __float_as_uint(f[u]);
             } else {
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int j = p * 32 + gq * 4 + e;
-                const int h = j >> 5, src = j & 31;
-                const float sw = __shfl_sync(0xffffffffu, swv[h], src);
-                const int32_t ws = __shfl_sync(0xffffffffu, wsv[h], src);
-                const float b = __shfl_sync(0xffffffffu, bv[h], src);
-                const int32_t a32 = static_cast<int32_t>(r[j]) - zx * ws;
-                if constexpr (kOut == kOutS32)
-                  packed[e] = static_cast<uint32_t>(a32);
-                else
-                  packed[e] = __float_as_uint(fmaf(static_cast<float>(a32), sx * sw, b));
-              }
+              for (int u = 0; u < 4; ++u) w[j4 + u] = static_cast<uint32_t>(a32[u]);
             }
-            *reinterpret_cast<uint4*>(stage + lane * 128 + ((gq ^ (lane & 7)) * 16)) =
-                make_uint4(packed[0], packed[1], packed[2], packed[3]);
           }
-          __syncwarp();
-          // coalesced write-out: 8 lanes per row (128 contiguous bytes), 4 rows per step
-          const int col0 = cb + p * cols_per_pass;
+          // stage: row `lane`, 4 granules of 16 B, 64-byte swizzle (conflict-free)
+          uint8_t* sb = stage + buf * (32 * 64);
+          if (g.tma_store) {
+            if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer 2 pieces ago
+            __syncwarp();
+          }
 #pragma unroll
-          for (int st = 0; st < 8; ++st) {
-            const int rr = st * 4 + (lane >> 3);
-            const int gq = lane & 7;
-            const int grow = m0 + q * 32 + rr;
-            const int gcol = col0 + gq * (16 / esize);
-            if (grow < g.M && gcol < g.N) {
-              const uint4 v = *reinterpret_cast<const uint4*>(stage + rr * 128 + ((gq ^ (rr & 7)) * 16));
-              uint8_t* dst = static_cast<uint8_t*>(g.y) + (static_cast<int64_t>(grow) * g.ldy + gcol) * esize;
-              if (g.vec_store && gcol + 16 / esize <= g.N) {
-                *reinterpret_cast<uint4*>(dst) = v;
-              } else {
-                const uint8_t* src = reinterpret_cast<const uint8_t*>(&v);
+          for (int gq = 0; gq < 4; ++gq)
+            *reinterpret_cast<uint4*>(sb + lane * 64 + ((gq ^ ((lane >> 1) & 3)) * 16)) =
+                make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
+          const int col0 = n0 + c * 32 + piece * kPieceCols;
+          if (g.tma_store) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmY, sb, col0 * esize, m0 + q * 32);
+              bulk_commit();
+            }
+            buf ^= 1;
+          } else {
+            __syncwarp();
+            // coalesced copy-out: 4 lanes per row (64 contiguous bytes), 8 rows per step
+#pragma unroll
+            for (int st = 0; st < 4; ++st) {
+              const int rr = st * 8 + (lane >> 2);
+              const int gq = lane & 3;
+              const int grow = m0 + q * 32 + rr;
+              const int gcol = col0 + gq * (16 / esize);
+              if (grow < g.M && gcol < g.N) {
+                const uint4 v =
+                    *reinterpret_cast<const uint4*>(sb + rr * 64 + ((gq ^ ((rr >> 1) & 3)) * 16));
+                uint8_t* dst = static_cast<uint8_t*>(g.y) +
+                               (static_cast<int64_t>(grow) * g.ldy + gcol) * esize;
+                const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
                 const int nel = min(16 / esize, g.N - gcol);
-                for (int b = 0; b < nel * esize; ++b) dst[b] = src[b];
+#pragma unroll
+                for (int b = 0; b < 16; ++b)
+                  if (b < nel * esize) dst[b] = static_cast<uint8_t>(vv[b >> 2] >> (8 * (b & 3)));
               }
             }
+            __syncwarp();
           }
-          __syncwarp();
         }
       }
     }
+    if (g.tma_store && lane == 0) bulk_wait<0>();
   } else if constexpr (kW4) {
     // ------------------------------------------------------------ nibble converters
     const int ct = threadIdx.x - 32 * (2 + kEpiWarps);  // 0..127

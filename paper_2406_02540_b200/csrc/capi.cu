@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -492,7 +493,12 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
   g.bias = kind == dtq_gemm::kOutS32 ? nullptr : h->bias_f;
   g.y = yk;
   g.ldy = ldk;
-  g.out_kind = kind;
+  // diagnostics: DTQ_DEBUG_GEMM_NOEPI=1 runs the main loop without an epilogue
+  static const bool noepi = [] {
+    const char* e = std::getenv("DTQ_DEBUG_GEMM_NOEPI");
+    return e && e[0] == '1';
+  }();
+  g.out_kind = noepi ? dtq_gemm::kOutNone : kind;
   g.tma_store = (reinterpret_cast<uintptr_t>(yk) % 16 == 0) && ((ldk * es) % 16 == 0);
   CUtensorMap tY;
   std::memset(&tY, 0, sizeof(tY));

@@ -52,7 +52,9 @@ cudaError_t dtq_launch_gemm_o(const CUtensorMap& tA, const CUtensorMap& tB,
       return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutBF16>(tA, tB, tY, g, sms, st);
     case dtq_gemm::kOutF32:
       return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutF32>(tA, tB, tY, g, sms, st);
-    default:
+    case dtq_gemm::kOutS32:
       return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutS32>(tA, tB, tY, g, sms, st);
+    default:
+      return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutNone>(tA, tB, tY, g, sms, st);
   }
 }

@@ -30,7 +30,13 @@
 
 namespace dtq_gemm {
 
-enum OutKind : int { kOutF16 = 0, kOutBF16 = 1, kOutF32 = 2, kOutS32 = 3 };
+enum OutKind : int {
+  kOutF16 = 0,
+  kOutBF16 = 1,
+  kOutF32 = 2,
+  kOutS32 = 3,
+  kOutNone = 4  // diagnostics only: drain TMEM without an epilogue (main-loop speed)
+};
 
 struct GemmArgs {
   int M, N, K;
@@ -48,15 +54,21 @@ struct GemmArgs {
 
 constexpr int BM = 128;
 constexpr int BK = 128;  // bytes (= int8 elements) per k-block: one 128-byte swizzle atom
-constexpr int kEpiWarps = 4;
 constexpr int kConvWarps = 4;
+// epilogue warps: 8 for W8A8 (two per TMEM lane quarter, each half of the
+// columns); 4 for W4A8, whose 4 converter warps take the remaining slots.
+template <bool kW4>
+__host__ __device__ constexpr int epi_warps() {
+  return kW4 ? 4 : 8;
+}
 
 template <int BN, int kStages, bool kW4>
 struct Smem {
   static constexpr int kA = BM * BK;                   // 16 KB
   static constexpr int kB = BN * BK;                   // s8 tile
   static constexpr int kP = kW4 ? BN * (BK / 2) : 0;   // packed nibbles
-  static constexpr int kEpi = kEpiWarps * 2 * 32 * 64;  // 2 x (32 rows x 64 B) per warp
+  static constexpr int kEpiBufs = kW4 ? 2 : 1;                  // staging buffers per warp
+  static constexpr int kEpi = epi_warps<kW4>() * kEpiBufs * 32 * 64;  // 32 rows x 64 B each
   static constexpr int kPar = 2 * 3 * BN * 4;             // {s_w, wsum, bias} x 2 tiles
   static constexpr int offA = 0;
   static constexpr int offB = offA + kStages * kA;
@@ -67,11 +79,12 @@ struct Smem {
   static constexpr int kBars = kStages * 3 + 4;
   static constexpr int bytes = offBar + kBars * 8 + 16;
   static constexpr int alloc = bytes + 1024;  // manual 1024-byte alignment
+  static_assert(alloc <= 227 * 1024, "shared memory budget exceeded");
 };
 
 template <int BN, bool kW4>
-constexpr int num_threads() {
-  return 32 * (2 + kEpiWarps + (kW4 ? kConvWarps : 0));
+__host__ __device__ constexpr int num_threads() {
+  return 32 * (2 + epi_warps<kW4>() + (kW4 ? kConvWarps : 0));
 }
 
 __device__ __forceinline__ uint32_t s4x8_to_s8x8_lo(uint32_t w) {
@@ -99,9 +112,11 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
   constexpr uint32_t kTmemCols = 2 * BN;
   constexpr uint32_t kIdesc = idesc_i8_u8s8(BM, BN);
 
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  constexpr int kEpiWarps = epi_warps<kW4>();
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for SWIZZLE_128B, kept as arithmetic on the shared
+  // array so every access below compiles to LDS/STS (not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem + L::offA;
   uint8_t* sB = smem + L::offB;
   uint8_t* sP = smem + L::offP;
@@ -194,11 +209,16 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     }
   } else if (warp < 2 + kEpiWarps) {
     // ------------------------------------------------------------ epilogue
-    // warp w owns TMEM lanes [32*(w%4), +32) = tile rows; lane = one row.
+    // warp w owns TMEM lanes [32*(w%4), +32) = tile rows (lane = one row) and
+    // one contiguous column range of the tile (BN / (kEpiWarps/4) columns).
     const uint32_t q = warp & 3;
-    const int et = threadIdx.x - 64;                  // 0..127 among epilogue threads
-    uint8_t* stage = sE + (warp - 2) * (2 * 32 * 64);  // ping-pong 32 x 64 B buffers
-    constexpr int esize = (kOut == kOutF16 || kOut == kOutBF16) ? 2 : 4;
+    constexpr int kColGroups = kEpiWarps / 4;
+    constexpr int kCols = BN / kColGroups;
+    const int cgrp = (warp - 2) / 4;
+    const int et = threadIdx.x - 64;                   // index among epilogue threads
+    constexpr int kBufs = L::kEpiBufs;
+    uint8_t* stage = sE + (warp - 2) * (kBufs * 32 * 64);  // 32 x 64 B staging buffer(s)
+    constexpr int esize = (kOut == kOutF16 || kOut == kOutBF16 || kOut == kOutNone) ? 2 : 4;
     constexpr int kPieceCols = 64 / esize;             // columns per 64-byte staged row
     int buf = 0;
     int it = 0;
@@ -225,15 +245,17 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int cl = 0; cl < kCols / 32; ++cl) {
+        const int c = cgrp * (kCols / 32) + cl;  // 32-column chunk index within the tile
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
-        if (c == BN / 32 - 1) {
+        if (cl == kCols / 32 - 1) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
+        if constexpr (kOut == kOutNone) continue;
 #pragma unroll
         for (int piece = 0; piece < 32 / kPieceCols; ++piece) {
           // 16 output words = 64 bytes of this row
@@ -277,7 +299,8 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
           // stage: row `lane`, 4 granules of 16 B, 64-byte swizzle (conflict-free)
           uint8_t* sb = stage + buf * (32 * 64);
           if (g.tma_store) {
-            if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer 2 pieces ago
+            // the bulk store that last read this buffer must have finished reading it
+            if (lane == 0) bulk_wait_read<kBufs - 1>();
             __syncwarp();
           }
 #pragma unroll
@@ -292,7 +315,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
               tma_store_2d(&tmY, sb, col0 * esize, m0 + q * 32);
               bulk_commit();
             }
-            buf ^= 1;
+            buf = (buf + 1) % kBufs;
           } else {
             __syncwarp();
             // coalesced copy-out: 4 lanes per row (64 contiguous bytes), 8 rows per step

@@ -331,7 +331,7 @@ struct dtq_qlinear_s {
   float* inv_smooth = nullptr;
   int8_t* signs = nullptr;    // [K] or null
   int hblock = 0;
-  CUtensorMap tmB;
+  CUtensorMap tmB[3];  // B operand boxes of 256, 128 and 64 rows
   // handle-owned scratch (forward without workspace, F64 output, host forward)
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -433,18 +433,50 @@ int finish_from_codes(dtq_qlinear_s* h, const uint8_t* codes, int64_t ldc, const
     to_f32_kernel<<<g, 256, 0, st>>>(h->bias, h->bias_f, N, 0);
     CUDA_TRY(cudaGetLastError());
   }
-  const int BN = N > 128 ? 256 : 128;
-  if (h->wbits == 8)
-    DTQ_TRY(make_tmap_u8(&h->tmB, h->w8, N, K, h->ld8, dtq_gemm::BK, BN,
-                         CU_TENSOR_MAP_SWIZZLE_128B));
-  else
-    DTQ_TRY(make_tmap_u8(&h->tmB, h->w4, N, (K + 1) / 2, h->ld4, dtq_gemm::BK / 2, BN,
-                         CU_TENSOR_MAP_SWIZZLE_NONE));
+  const int rows[3] = {256, 128, 64};
+  for (int i = 0; i < 3; ++i) {
+    if (h->wbits == 8)
+      DTQ_TRY(make_tmap_u8(&h->tmB[i], h->w8, N, K, h->ld8, dtq_gemm::BK, rows[i],
+                           CU_TENSOR_MAP_SWIZZLE_128B));
+    else
+      DTQ_TRY(make_tmap_u8(&h->tmB[i], h->w4, N, (K + 1) / 2, h->ld4, dtq_gemm::BK / 2, rows[i],
+                           CU_TENSOR_MAP_SWIZZLE_NONE));
+  }
   return DTQ_OK;
 }
 
 // ------------------------------------------------------------------ GEMM launch
 // (kernel instantiations live in gemm_w8.cu / gemm_w4.cu)
+// Tile configuration: minimise (waves x per-SM tile width) over the candidate
+// shapes; ties go to the CTA pair (half the B traffic per SM) and wider N.
+// DTQ_GEMM_CFG=<0..3> forces {1cta/256, 1cta/128, 2cta/256, 2cta/128}.
+GemmCfg choose_gemm_cfg(int64_t M, int64_t N, int wbits, int sms) {
+  const GemmCfg cands[4] = {{256, 1}, {128, 1}, {256, 0}, {128, 0}};
+  static const int forced = [] {
+    const char* e = std::getenv("DTQ_GEMM_CFG");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (forced >= 0 && forced < 4) {
+    const GemmCfg f[4] = {{256, 0}, {128, 0}, {256, 1}, {128, 1}};
+    if (!(wbits == 4 && f[forced].cta2)) return f[forced];
+  }
+  GemmCfg best{256, 0};
+  int64_t best_cost = INT64_MAX;
+  for (const GemmCfg& c : cands) {
+    if (c.cta2 && wbits == 4) continue;
+    const int64_t tm = c.cta2 ? 256 : 128;
+    const int64_t tiles = ((M + tm - 1) / tm) * ((N + c.bn - 1) / c.bn);
+    const int64_t units = c.cta2 ? sms / 2 : sms;
+    const int64_t waves = (tiles + units - 1) / units;
+    const int64_t cost = waves * c.bn;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = c;
+    }
+  }
+  return best;
+}
+
 int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32_t* z_x,
                int64_t M, dtq_qlinear_s* h, void* y, int y_dtype, int64_t ldy, cudaStream_t st) {
   if (!h) return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: null handle");
@@ -454,7 +486,12 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
   if (M > INT32_MAX / 2) return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: M too large");
   DTQ_TRY(overflow_check(h->abits, h->wbits, h->K));
   DTQ_TRY(check_device());
-  const int BN = h->N > 128 ? 256 : 128;
+  const int sms = device_info().sms;
+  const GemmCfg cfg = choose_gemm_cfg(M, h->N, h->wbits, sms);
+  const int BN = cfg.bn;
+  const int tile_m = cfg.cta2 ? 2 * dtq_gemm::BM : dtq_gemm::BM;
+  const int brows = cfg.cta2 ? BN / 2 : BN;
+  const CUtensorMap& tB = h->tmB[brows == 256 ? 0 : (brows == 128 ? 1 : 2)];
 
   CUtensorMap tA;
   DTQ_TRY(make_tmap_u8(&tA, codes, M, h->K, ldc, dtq_gemm::BK, dtq_gemm::BM,
@@ -483,7 +520,7 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
   g.M = static_cast<int>(M);
   g.N = static_cast<int>(h->N);
   g.K = static_cast<int>(h->K);
-  g.tiles_m = static_cast<int>((M + dtq_gemm::BM - 1) / dtq_gemm::BM);
+  g.tiles_m = static_cast<int>((M + tile_m - 1) / tile_m);
   g.tiles_n = static_cast<int>((h->N + BN - 1) / BN);
   g.k_blocks = static_cast<int>((h->K + dtq_gemm::BK - 1) / dtq_gemm::BK);
   g.s_x = s_x;
@@ -506,9 +543,8 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
     DTQ_TRY(make_tmap_u8(&tY, yk, M, h->N * static_cast<int64_t>(es), ldk * es, 64, 32,
                          CU_TENSOR_MAP_SWIZZLE_64B));
 
-  const int sms = device_info().sms;
-  const cudaError_t e = h->wbits == 8 ? dtq_launch_gemm_w8(tA, h->tmB, tY, g, BN, sms, st)
-                                      : dtq_launch_gemm_w4(tA, h->tmB, tY, g, BN, sms, st);
+  const cudaError_t e = h->wbits == 8 ? dtq_launch_gemm_w8(tA, tB, tY, g, cfg, sms, st)
+                                      : dtq_launch_gemm_w4(tA, tB, tY, g, BN, sms, st);
   if (e != cudaSuccess) return fail(DTQ_ERR_CUDA, "qgemm launch: %s", cudaGetErrorString(e));
 
   if (y_dtype == DTQ_F64) {

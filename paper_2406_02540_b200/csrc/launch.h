@@ -12,20 +12,25 @@
 cudaError_t dtq_launch_fq(const dtq_fq::FqArgs& a, int x_dtype, bool exact, int cpt, bool vec,
                           int block, int sms, cudaStream_t st);
 
-// tcgen05 integer GEMM; BN in {128, 256}
+// tcgen05 integer GEMM tile configurations
+struct GemmCfg {
+  int bn;    // 128 or 256
+  int cta2;  // 1: CTA pair (256-row tiles, cta_group::2)
+};
+// tcgen05 integer GEMM (W8A8)
 cudaError_t dtq_launch_gemm_w8(const CUtensorMap& tA, const CUtensorMap& tB,
-                               const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, int BN, int sms,
-                               cudaStream_t st);
+                               const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, GemmCfg c,
+                               int sms, cudaStream_t st);
 cudaError_t dtq_launch_gemm_w4(const CUtensorMap& tA, const CUtensorMap& tB,
                                const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, int BN, int sms,
                                cudaStream_t st);
 
-template <int BN, int kStages, bool kW4, int kOut>
+template <int BN, int kStages, bool kW4, int kOut, bool k2Cta>
 cudaError_t dtq_launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB,
                               const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, int sms,
                               cudaStream_t st) {
-  using L = dtq_gemm::Smem<BN, kStages, kW4>;
-  auto kern = dtq_gemm::qgemm_kernel<BN, kStages, kW4, kOut>;
+  using L = dtq_gemm::Smem<BN, kStages, kW4, k2Cta>;
+  auto kern = dtq_gemm::qgemm_kernel<BN, kStages, kW4, kOut, k2Cta>;
   static thread_local int configured_dev = -1;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -36,25 +41,38 @@ cudaError_t dtq_launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB,
     configured_dev = dev;
   }
   const int tiles = g.tiles_m * g.tiles_n;
-  const int grid = tiles < sms ? tiles : sms;
-  kern<<<grid, dtq_gemm::num_threads<BN, kW4>(), L::alloc, st>>>(tA, tB, tY, g);
-  return cudaGetLastError();
+  const int per = k2Cta ? 2 : 1;                   // CTAs per tile
+  const int units = sms / per;
+  const int grid = per * (tiles < units ? tiles : units);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(dtq_gemm::num_threads<BN, kW4>());
+  cfg.dynamicSmemBytes = L::alloc;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = per;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tA, tB, tY, g);
 }
 
-template <int BN, int kStages, bool kW4>
+template <int BN, int kStages, bool kW4, bool k2Cta>
 cudaError_t dtq_launch_gemm_o(const CUtensorMap& tA, const CUtensorMap& tB,
                               const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, int sms,
                               cudaStream_t st) {
   switch (g.out_kind) {
     case dtq_gemm::kOutF16:
-      return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutF16>(tA, tB, tY, g, sms, st);
+      return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutF16, k2Cta>(tA, tB, tY, g, sms, st);
     case dtq_gemm::kOutBF16:
-      return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutBF16>(tA, tB, tY, g, sms, st);
+      return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutBF16, k2Cta>(tA, tB, tY, g, sms, st);
     case dtq_gemm::kOutF32:
-      return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutF32>(tA, tB, tY, g, sms, st);
+      return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutF32, k2Cta>(tA, tB, tY, g, sms, st);
     case dtq_gemm::kOutS32:
-      return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutS32>(tA, tB, tY, g, sms, st);
+      return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutS32, k2Cta>(tA, tB, tY, g, sms, st);
     default:
-      return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutNone>(tA, tB, tY, g, sms, st);
+      return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutNone, k2Cta>(tA, tB, tY, g, sms, st);
   }
 }

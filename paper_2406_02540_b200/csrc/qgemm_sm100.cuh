@@ -62,10 +62,11 @@ __host__ __device__ constexpr int epi_warps() {
   return kW4 ? 4 : 8;
 }
 
-template <int BN, int kStages, bool kW4>
+template <int BN, int kStages, bool kW4, bool k2Cta = false>
 struct Smem {
-  static constexpr int kA = BM * BK;                   // 16 KB
-  static constexpr int kB = BN * BK;                   // s8 tile
+  static constexpr int kA = BM * BK;                   // 16 KB (this CTA's 128 rows)
+  static constexpr int kBRows = k2Cta ? BN / 2 : BN;   // a CTA pair splits B along N
+  static constexpr int kB = kBRows * BK;               // s8 tile
   static constexpr int kP = kW4 ? BN * (BK / 2) : 0;   // packed nibbles
   static constexpr int kEpiBufs = kW4 ? 2 : 1;                  // staging buffers per warp
   static constexpr int kEpi = epi_warps<kW4>() * kEpiBufs * 32 * 64;  // 32 rows x 64 B each
@@ -103,14 +104,23 @@ __device__ __forceinline__ uint32_t s4x8_to_s8x8_hi(uint32_t w) {
   return e | ((e & 0x08080808u) * 0x1Eu);
 }
 
-template <int BN, int kStages, bool kW4, int kOut>
+// k2Cta: a cluster of two CTAs on one TPC computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2 issued by the leader (rank 0).  Each CTA loads its
+// own 128 rows of A and half of the B rows; both TMA streams complete on the
+// leader's `full` barrier, and the leader's MMA commits are multicast to the
+// `empty` / `tfull` barriers of both CTAs.  Each CTA's TMEM holds its 128
+// accumulator rows, drained by its own epilogue warps, which release the
+// buffer on the leader's `tempty` barrier.
+template <int BN, int kStages, bool kW4, int kOut, bool k2Cta>
 __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     qgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmY, const GemmArgs g) {
   using namespace dtq_ptx;
-  using L = Smem<BN, kStages, kW4>;
+  static_assert(!(kW4 && k2Cta), "W4A8 runs on the single-CTA kernel");
+  using L = Smem<BN, kStages, kW4, k2Cta>;
   constexpr uint32_t kTmemCols = 2 * BN;
-  constexpr uint32_t kIdesc = idesc_i8_u8s8(BM, BN);
+  constexpr int kTileM = k2Cta ? 2 * BM : BM;
+  constexpr uint32_t kIdesc = idesc_i8_u8s8(kTileM, BN);
 
   constexpr int kEpiWarps = epi_warps<kW4>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -132,6 +142,9 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const int total_tiles = g.tiles_m * g.tiles_n;
+  const uint32_t rank = k2Cta ? cluster_ctarank() : 0;  // CTA rank in the pair
+  const int tile0 = k2Cta ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int tstride = k2Cta ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -144,13 +157,21 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps);
+      mbar_init(&tempty[i], kEpiWarps * (k2Cta ? 2 : 1));
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (k2Cta)
+      tmem_alloc_cta2<kTmemCols>(tmem_slot);
+    else
+      tmem_alloc<kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (k2Cta)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -159,17 +180,25 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        const int m0 = (tile % g.tiles_m) * BM;
+      for (int tile = tile0; tile < total_tiles; tile += tstride) {
+        const int m0 = (tile % g.tiles_m) * kTileM + rank * BM;
         const int n0 = (tile / g.tiles_m) * BN;
         for (int kb = 0; kb < g.k_blocks; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], L::kA + (kW4 ? L::kP : L::kB));
-          tma_load_2d(sA + s * L::kA, &tmA, &full[s], kb * BK, m0);
-          if constexpr (kW4)
-            tma_load_2d(sP + s * L::kP, &tmB, &full[s], kb * (BK / 2), n0);
-          else
-            tma_load_2d(sB + s * L::kB, &tmB, &full[s], kb * BK, n0);
+          if constexpr (k2Cta) {
+            // both CTAs' bytes land on the leader's barrier; only it arms it
+            const uint32_t lead_full = mapa_shared(smem_u32(&full[s]), 0);
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (L::kA + L::kB));
+            tma_load_2d_2sm(sA + s * L::kA, &tmA, lead_full, kb * BK, m0);
+            tma_load_2d_2sm(sB + s * L::kB, &tmB, lead_full, kb * BK, n0 + rank * L::kBRows);
+          } else {
+            mbar_arrive_expect_tx(&full[s], L::kA + (kW4 ? L::kP : L::kB));
+            tma_load_2d(sA + s * L::kA, &tmA, &full[s], kb * BK, m0);
+            if constexpr (kW4)
+              tma_load_2d(sP + s * L::kP, &tmB, &full[s], kb * (BK / 2), n0);
+            else
+              tma_load_2d(sB + s * L::kB, &tmB, &full[s], kb * BK, n0);
+          }
           if (++s == kStages) {
             s = 0;
             ph ^= 1;
@@ -179,11 +208,11 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+      for (int tile = tile0; tile < total_tiles; tile += tstride, ++it) {
         const int acc = it & 1;
         const uint32_t aph = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
@@ -196,15 +225,25 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
           const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * L::kA));
           const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * L::kB));
 #pragma unroll
-          for (int k = 0; k < BK / 32; ++k)
-            mma_i8(d, ad + 2 * k, bd + 2 * k, kIdesc, (kb | k) != 0 ? 1u : 0u);
-          mma_commit(&empty[s]);
+          for (int k = 0; k < BK / 32; ++k) {
+            if constexpr (k2Cta)
+              mma_i8_cta2(d, ad + 2 * k, bd + 2 * k, kIdesc, (kb | k) != 0 ? 1u : 0u);
+            else
+              mma_i8(d, ad + 2 * k, bd + 2 * k, kIdesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          if constexpr (k2Cta)
+            mma_commit_cta2_mc(&empty[s], 0x3);
+          else
+            mma_commit(&empty[s]);
           if (++s == kStages) {
             s = 0;
             ph ^= 1;
           }
         }
-        mma_commit(&tfull[acc]);
+        if constexpr (k2Cta)
+          mma_commit_cta2_mc(&tfull[acc], 0x3);
+        else
+          mma_commit(&tfull[acc]);
       }
     }
   } else if (warp < 2 + kEpiWarps) {
@@ -222,10 +261,10 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     constexpr int kPieceCols = 64 / esize;             // columns per 64-byte staged row
     int buf = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+    for (int tile = tile0; tile < total_tiles; tile += tstride, ++it) {
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
-      const int m0 = (tile % g.tiles_m) * BM;
+      const int m0 = (tile % g.tiles_m) * kTileM + rank * BM;
       const int n0 = (tile / g.tiles_m) * BN;
       // per-column params of this tile -> smem (overlaps the tile's main loop)
       uint32_t* par = sPar + acc * (3 * BN);
@@ -253,7 +292,12 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         if (cl == kCols / 32 - 1) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) {
+            if constexpr (k2Cta)
+              mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+            else
+              mbar_arrive(&tempty[acc]);
+          }
         }
         if constexpr (kOut == kOutNone) continue;
 #pragma unroll
@@ -275,8 +319,18 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
             for (int u = 0; u < 4; ++u) {
               const int j = piece * kPieceCols + j4 + u;
               a32[u] = static_cast<int32_t>(r[j]) - zx * static_cast<int32_t>(wsv[u]);
-              f[u] = fmaf(static_cast<float>(a32[u]), sx * __uint_as_float(swv[u]),
-                          __uint_as_float(bv[u]));
+            }
+            // dequant in packed fp32x2 (FMUL2 / FFMA2): y = acc * (s_x * s_w) + bias
+#pragma unroll
+            for (int u = 0; u < 4; u += 2) {
+              const float2 sc = __fmul2_rn(make_float2(sx, sx),
+                                           make_float2(__uint_as_float(swv[u]),
+                                                       __uint_as_float(swv[u + 1])));
+              const float2 yy = __ffma2_rn(
+                  make_float2(static_cast<float>(a32[u]), static_cast<float>(a32[u + 1])), sc,
+                  make_float2(__uint_as_float(bv[u]), __uint_as_float(bv[u + 1])));
+              f[u] = yy.x;
+              f[u + 1] = yy.y;
             }
             if constexpr (kOut == kOutF16) {
               const __half2 h0 = __floats2half2_rn(f[0], f[1]);
@@ -348,7 +402,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     const int ct = threadIdx.x - 32 * (2 + kEpiWarps);  // 0..127
     int s = 0;
     uint32_t ph = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int tile = tile0; tile < total_tiles; tile += tstride) {
       for (int kb = 0; kb < g.k_blocks; ++kb) {
         mbar_wait(&full[s], ph);
         const uint8_t* src = sP + s * L::kP;
@@ -374,10 +428,16 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (k2Cta)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<kTmemCols>(tmem_base);
+    if constexpr (k2Cta)
+      tmem_dealloc_cta2<kTmemCols>(tmem_base);
+    else
+      tmem_dealloc<kTmemCols>(tmem_base);
   }
 }
 

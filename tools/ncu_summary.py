@@ -12,7 +12,7 @@ METRICS = ["Duration", "Elapsed Cycles", "SM Frequency", "DRAM Throughput", "Mem
 
 
 def run(args):
-    return subprocess.run(["ncu", "-i", *args], capture_output=True, text=True).stdout
+    return subprocess.run(["ncu", "-i", *args, "--print-units", "base"], capture_output=True, text=True).stdout
 
 
 def details(rep):

@@ -477,6 +477,19 @@ GemmCfg choose_gemm_cfg(int64_t M, int64_t N, int wbits, int sms) {
   return best;
 }
 
+// diagnostics: device buffer of per-CTA wait-cycle counters, allocated only
+// when DTQ_DEBUG_GEMM_PROBE=1 (read back with dtq_diag_probe_ptr)
+unsigned long long* probe_buffer() {
+  static unsigned long long* p = [] {
+    const char* e = std::getenv("DTQ_DEBUG_GEMM_PROBE");
+    unsigned long long* b = nullptr;
+    if (e && e[0] == '1' && cudaMalloc(&b, 4096 * 8 * 8) == cudaSuccess)
+      cudaMemset(b, 0, 4096 * 8 * 8);
+    return b;
+  }();
+  return p;
+}
+
 int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32_t* z_x,
                int64_t M, dtq_qlinear_s* h, void* y, int y_dtype, int64_t ldy, cudaStream_t st) {
   if (!h) return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: null handle");
@@ -536,7 +549,18 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
     return e && e[0] == '1';
   }();
   g.out_kind = noepi ? dtq_gemm::kOutNone : kind;
-  g.tma_store = (reinterpret_cast<uintptr_t>(yk) % 16 == 0) && ((ldk * es) % 16 == 0);
+  static const int dbg = [] {
+    const char* e = std::getenv("DTQ_DEBUG_GEMM_EPI");
+    return e ? std::atoi(e) : 0;
+  }();
+  g.dbg = dbg;
+  g.probe = probe_buffer();
+  static const bool no_tma_store = [] {
+    const char* e = std::getenv("DTQ_DEBUG_NO_TMA_STORE");
+    return e && e[0] == '1';
+  }();
+  g.tma_store = !no_tma_store && (reinterpret_cast<uintptr_t>(yk) % 16 == 0) &&
+                ((ldk * es) % 16 == 0);
   CUtensorMap tY;
   std::memset(&tY, 0, sizeof(tY));
   if (g.tma_store)
@@ -601,6 +625,9 @@ const char* dtq_last_error(void) { return g_last_error.c_str(); }
 int dtq_capi_version(void) { return DTQ_CAPI_VERSION; }
 
 int dtq_device_check(void) { return check_device(); }
+
+// diagnostics only (deliberately not declared in include/dtq_capi.h)
+void* dtq_diag_probe_ptr(void) { return probe_buffer(); }
 
 int dtq_quantize_rows(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx,
                       int bits, int symmetric, int mode, const dtq_balance* balance,

@@ -5,17 +5,18 @@
 //   acc     -= z_x[t] * sum_c w_s8[o,c]                   (qgemm.cpp:60)
 //   y[t,o]   = s_x[t] * s_w[o] * acc + bias[o]            (qgemm.cpp:61-63)
 //
-// Persistent, warp-specialised, one CTA per SM:
-//   warp 0      TMA producer: A tile 128 x 128 B and B tile BN x 128 B per
-//               k-block into a kStages ring (SWIZZLE_128B, mbarrier tx-count)
-//   warp 1      TMEM allocator + single-thread MMA issuer (4 x K=32 MMAs per
-//               k-block), tcgen05.commit frees smem stages and publishes a
+// Persistent, warp-specialised, one CTA (or CTA pair) per SM:
+//   epilogue warps (8 for W8A8, 4 for W4A8; low warp ids): tcgen05.ld 32
+//               TMEM lanes x 32 columns, zero-point correction + dequant
+//               (packed fp32x2) + bias + cast, swizzled smem staging, TMA
+//               bulk stores (or coalesced 128-bit stores for unaligned y)
+//   converter warps (W4A8 only): packed [BN x 64 B] nibbles -> s8 in the
+//               canonical SWIZZLE_128B K-major layout
+//   TMA warp    producer: A tile 128 x 128 B and B tile BN x 128 B (or BN/2
+//               rows per CTA of a pair) per k-block into a kStages ring
+//   MMA warp    TMEM allocator + single-thread MMA issuer (4 x K=32 MMAs per
+//               k-block); tcgen05.commit frees smem stages and publishes a
 //               finished accumulator
-//   warps 2..5  epilogue: tcgen05.ld 32 lanes x 64 columns, zero-point
-//               correction + dequant + bias + cast, swizzled smem staging,
-//               coalesced 128-bit global stores
-//   warps 6..9  (W4A8 only) nibble converters: packed [BN x 64 B] stage ->
-//               s8 in the canonical SWIZZLE_128B K-major layout
 // TMEM holds two BN-column s32 accumulators so the epilogue of tile i
 // overlaps the main loop of tile i+1.
 #pragma once
@@ -50,6 +51,9 @@ struct GemmArgs {
   int64_t ldy;          // elements
   int out_kind;
   int tma_store;        // 1: y rows 16-byte aligned -> TMA bulk stores (tmY valid)
+  unsigned long long* probe;  // diagnostics: per-CTA wait-cycle counters (or nullptr)
+  int dbg;              // diagnostics: 0 full epilogue, 2 TMEM loads only,
+                        // 3 loads + dequant math, 4 + smem staging (no stores)
 };
 
 constexpr int BM = 128;
@@ -68,7 +72,7 @@ struct Smem {
   static constexpr int kBRows = k2Cta ? BN / 2 : BN;   // a CTA pair splits B along N
   static constexpr int kB = kBRows * BK;               // s8 tile
   static constexpr int kP = kW4 ? BN * (BK / 2) : 0;   // packed nibbles
-  static constexpr int kEpiBufs = kW4 ? 2 : 1;                  // staging buffers per warp
+  static constexpr int kEpiBufs = 2;                             // staging buffers per warp
   static constexpr int kEpi = epi_warps<kW4>() * kEpiBufs * 32 * 64;  // 32 rows x 64 B each
   static constexpr int kPar = 2 * 3 * BN * 4;             // {s_w, wsum, bias} x 2 tiles
   static constexpr int offA = 0;
@@ -139,14 +143,31 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
+  // Warp roles.  The SM's warp arbiter favours higher warp ids, so the
+  // latency-critical single-thread roles (TMA producer, MMA issuer) take the
+  // two highest ids and the epilogue / converter warps the low ones.
+  constexpr uint32_t kTmaWarp = kEpiWarps + (kW4 ? kConvWarps : 0);
+  constexpr uint32_t kMmaWarp = kTmaWarp + 1;
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const int total_tiles = g.tiles_m * g.tiles_n;
   const uint32_t rank = k2Cta ? cluster_ctarank() : 0;  // CTA rank in the pair
+  // diagnostics: cycles spent in each role's waits (DTQ_DEBUG_GEMM_PROBE)
+  unsigned long long pw0 = 0, pw1 = 0;
+  auto timed_wait = [&](uint64_t* bar, uint32_t par, unsigned long long& acc_cycles) {
+    if (g.probe == nullptr) {
+      mbar_wait(bar, par);
+      return;
+    }
+    const long long t0 = clock64();
+    mbar_wait(bar, par);
+    acc_cycles += static_cast<unsigned long long>(clock64() - t0);
+  };
   const int tile0 = k2Cta ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
   const int tstride = k2Cta ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
 
-  if (warp == 0 && lane == 0) {
+  const long long t_start = clock64();
+  if (warp == kTmaWarp && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     if (g.tma_store) prefetch_tmap(&tmY);
@@ -161,7 +182,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     if constexpr (k2Cta)
       tmem_alloc_cta2<kTmemCols>(tmem_slot);
     else
@@ -175,7 +196,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int s = 0;
@@ -184,7 +205,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         const int m0 = (tile % g.tiles_m) * kTileM + rank * BM;
         const int n0 = (tile / g.tiles_m) * BN;
         for (int kb = 0; kb < g.k_blocks; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
+          timed_wait(&empty[s], ph ^ 1, pw0);
           if constexpr (k2Cta) {
             // both CTAs' bytes land on the leader's barrier; only it arms it
             const uint32_t lead_full = mapa_shared(smem_u32(&full[s]), 0);
@@ -206,7 +227,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0 && rank == 0) {
       int s = 0;
@@ -215,11 +236,11 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       for (int tile = tile0; tile < total_tiles; tile += tstride, ++it) {
         const int acc = it & 1;
         const uint32_t aph = (it >> 1) & 1;
-        mbar_wait(&tempty[acc], aph ^ 1);
+        timed_wait(&tempty[acc], aph ^ 1, pw1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
         for (int kb = 0; kb < g.k_blocks; ++kb) {
-          mbar_wait(&full[s], ph);
+          timed_wait(&full[s], ph, pw0);
           if constexpr (kW4) mbar_wait(&conv[s], ph);
           tc_fence_after();
           const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * L::kA));
@@ -246,50 +267,80 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
           mma_commit(&tfull[acc]);
       }
     }
-  } else if (warp < 2 + kEpiWarps) {
+  } else if (warp < kEpiWarps) {
     // ------------------------------------------------------------ epilogue
     // warp w owns TMEM lanes [32*(w%4), +32) = tile rows (lane = one row) and
     // one contiguous column range of the tile (BN / (kEpiWarps/4) columns).
     const uint32_t q = warp & 3;
     constexpr int kColGroups = kEpiWarps / 4;
     constexpr int kCols = BN / kColGroups;
-    const int cgrp = (warp - 2) / 4;
-    const int et = threadIdx.x - 64;                   // index among epilogue threads
+    const int cgrp = warp / 4;
+    const int et = threadIdx.x;                        // index among epilogue threads
     constexpr int kBufs = L::kEpiBufs;
-    uint8_t* stage = sE + (warp - 2) * (kBufs * 32 * 64);  // 32 x 64 B staging buffer(s)
+    uint8_t* stage = sE + warp * (kBufs * 32 * 64);  // 32 x 64 B staging buffer(s)
     constexpr int esize = (kOut == kOutF16 || kOut == kOutBF16 || kOut == kOutNone) ? 2 : 4;
     constexpr int kPieceCols = 64 / esize;             // columns per 64-byte staged row
     int buf = 0;
     int it = 0;
+    // Per-column {s_w, -wsum, bias} and per-row {s_x, z_x} of the NEXT tile are
+    // fetched into registers while the current tile is processed, then parked
+    // in a double-buffered smem table: their global latency never stalls the
+    // drain of TMEM.
+    constexpr int kParPer = (BN + 32 * kEpiWarps - 1) / (32 * kEpiWarps);
+    uint32_t p_sw[kParPer], p_ws[kParPer], p_b[kParPer];
+    float nsx = 0.f;
+    int32_t nzx = 0;
+    auto fetch = [&](int t) {
+      const int tm0 = (t % g.tiles_m) * kTileM + rank * BM;
+      const int tn0 = (t / g.tiles_m) * BN;
+#pragma unroll
+      for (int i = 0; i < kParPer; ++i) {
+        const int col = tn0 + et + i * 32 * kEpiWarps;
+        const bool okc = col < g.N && et + i * 32 * kEpiWarps < BN;
+        p_sw[i] = __float_as_uint(okc ? __ldg(g.s_w + col) : 0.f);
+        p_ws[i] = static_cast<uint32_t>(okc ? -__ldg(g.wsum + col) : 0);
+        p_b[i] = __float_as_uint((okc && g.bias) ? __ldg(g.bias + col) : 0.f);
+      }
+      const int row = tm0 + q * 32 + lane;
+      nsx = row < g.M ? static_cast<float>(__ldg(g.s_x + row)) : 0.f;
+      nzx = row < g.M ? __ldg(g.z_x + row) : 0;
+    };
+    if (tile0 < total_tiles) fetch(tile0);
     for (int tile = tile0; tile < total_tiles; tile += tstride, ++it) {
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       const int m0 = (tile % g.tiles_m) * kTileM + rank * BM;
       const int n0 = (tile / g.tiles_m) * BN;
-      // per-column params of this tile -> smem (overlaps the tile's main loop)
       uint32_t* par = sPar + acc * (3 * BN);
-      for (int c = et; c < BN; c += 32 * kEpiWarps) {
-        const int col = n0 + c;
-        const bool okc = col < g.N;
-        par[c] = __float_as_uint(okc ? __ldg(g.s_w + col) : 0.f);
-        par[BN + c] = static_cast<uint32_t>(okc ? __ldg(g.wsum + col) : 0);
-        par[2 * BN + c] = __float_as_uint((okc && g.bias) ? __ldg(g.bias + col) : 0.f);
+#pragma unroll
+      for (int i = 0; i < kParPer; ++i) {
+        const int c = et + i * 32 * kEpiWarps;
+        if (c < BN) {
+          par[c] = p_sw[i];
+          par[BN + c] = p_ws[i];
+          par[2 * BN + c] = p_b[i];
+        }
       }
+      const float sx = nsx;
+      const int32_t zx = nzx;
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-      const int row = m0 + q * 32 + lane;
-      const bool row_ok = row < g.M;
-      const float sx = row_ok ? static_cast<float>(g.s_x[row]) : 0.f;
-      const int32_t zx = row_ok ? g.z_x[row] : 0;
+      if (tile + tstride < total_tiles) fetch(tile + tstride);
 
-      mbar_wait(&tfull[acc], aph);
+      timed_wait(&tfull[acc], aph, pw0);
       tc_fence_after();
-#pragma unroll 1
+      // TMEM -> registers, 32 columns at a time; chunk cl+1 is in flight while
+      // chunk cl is dequantised and stored (two register sets, full unroll)
+      const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * BN + cgrp * kCols;
+      uint32_t rr[2][32];
+      tmem_ld_32x32b_x32(tbase, rr[0]);
+      tmem_ld_wait_regs(rr[0]);
+#pragma unroll
       for (int cl = 0; cl < kCols / 32; ++cl) {
         const int c = cgrp * (kCols / 32) + cl;  // 32-column chunk index within the tile
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + c * 32, r);
-        tmem_ld_wait();
+        uint32_t (&r)[32] = rr[cl & 1];
+        if (cl + 1 < kCols / 32) tmem_ld_32x32b_x32(tbase + (cl + 1) * 32, rr[(cl + 1) & 1]);
         if (cl == kCols / 32 - 1) {
+          // every TMEM read of this accumulator has completed: hand it back
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -299,7 +350,10 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
               mbar_arrive(&tempty[acc]);
           }
         }
-        if constexpr (kOut == kOutNone) continue;
+        if (kOut == kOutNone || g.dbg == 2) {
+          if (cl + 1 < kCols / 32) tmem_ld_wait_regs(rr[(cl + 1) & 1]);
+          continue;
+        }
 #pragma unroll
         for (int piece = 0; piece < 32 / kPieceCols; ++piece) {
           // 16 output words = 64 bytes of this row
@@ -318,7 +372,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int j = piece * kPieceCols + j4 + u;
-              a32[u] = static_cast<int32_t>(r[j]) - zx * static_cast<int32_t>(wsv[u]);
+              a32[u] = static_cast<int32_t>(r[j]) + zx * static_cast<int32_t>(wsv[u]);  // -wsum
             }
             // dequant in packed fp32x2 (FMUL2 / FFMA2): y = acc * (s_x * s_w) + bias
 #pragma unroll
@@ -350,11 +404,36 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
               for (int u = 0; u < 4; ++u) w[j4 + u] = static_cast<uint32_t>(a32[u]);
             }
           }
+          if (g.dbg == 3) {  // diagnostics: keep the math alive, skip staging + stores
+            uint32_t x = 0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) x ^= w[i];
+            if (x == 0x9E3779B9u && lane == 77) static_cast<uint32_t*>(g.y)[0] = x;
+            continue;
+          }
+          if (g.dbg == 6) {  // diagnostics: direct 128-bit stores from registers, no staging
+            const int col0d = n0 + c * 32 + piece * kPieceCols;
+            const int rowd = m0 + q * 32 + lane;
+            if (rowd < g.M) {
+              uint8_t* dst = static_cast<uint8_t*>(g.y) +
+                             (static_cast<int64_t>(rowd) * g.ldy + col0d) * esize;
+#pragma unroll
+              for (int gq = 0; gq < 4; ++gq)
+                if (col0d + (gq + 1) * (16 / esize) <= g.N)
+                  *reinterpret_cast<uint4*>(dst + 16 * gq) =
+                      make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
+            }
+            continue;
+          }
           // stage: row `lane`, 4 granules of 16 B, 64-byte swizzle (conflict-free)
           uint8_t* sb = stage + buf * (32 * 64);
           if (g.tma_store) {
             // the bulk store that last read this buffer must have finished reading it
-            if (lane == 0) bulk_wait_read<kBufs - 1>();
+            if (lane == 0) {
+              const long long t0 = g.probe ? clock64() : 0;
+              bulk_wait_read<kBufs - 1>();
+              if (g.probe) pw1 += static_cast<unsigned long long>(clock64() - t0);
+            }
             __syncwarp();
           }
 #pragma unroll
@@ -362,6 +441,10 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
             *reinterpret_cast<uint4*>(sb + lane * 64 + ((gq ^ ((lane >> 1) & 3)) * 16)) =
                 make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
           const int col0 = n0 + c * 32 + piece * kPieceCols;
+          if (g.dbg == 4) {  // diagnostics: staging written, no global stores
+            __syncwarp();
+            continue;
+          }
           if (g.tma_store) {
             fence_proxy_async_smem();
             __syncwarp();
@@ -375,31 +458,35 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
             // coalesced copy-out: 4 lanes per row (64 contiguous bytes), 8 rows per step
 #pragma unroll
             for (int st = 0; st < 4; ++st) {
-              const int rr = st * 8 + (lane >> 2);
+              const int srow = st * 8 + (lane >> 2);
               const int gq = lane & 3;
-              const int grow = m0 + q * 32 + rr;
+              const int grow = m0 + q * 32 + srow;
               const int gcol = col0 + gq * (16 / esize);
               if (grow < g.M && gcol < g.N) {
                 const uint4 v =
-                    *reinterpret_cast<const uint4*>(sb + rr * 64 + ((gq ^ ((rr >> 1) & 3)) * 16));
+                    *reinterpret_cast<const uint4*>(sb + srow * 64 + ((gq ^ ((srow >> 1) & 3)) * 16));
                 uint8_t* dst = static_cast<uint8_t*>(g.y) +
                                (static_cast<int64_t>(grow) * g.ldy + gcol) * esize;
-                const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
                 const int nel = min(16 / esize, g.N - gcol);
-#pragma unroll
-                for (int b = 0; b < 16; ++b)
-                  if (b < nel * esize) dst[b] = static_cast<uint8_t>(vv[b >> 2] >> (8 * (b & 3)));
+                if (nel == 16 / esize && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                  *reinterpret_cast<uint4*>(dst) = v;
+                } else {
+                  const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+                  for (int b = 0; b < nel * esize; ++b)
+                    dst[b] = static_cast<uint8_t>(vv[b >> 2] >> (8 * (b & 3)));
+                }
               }
             }
             __syncwarp();
           }
         }
+        if (cl + 1 < kCols / 32) tmem_ld_wait_regs(rr[(cl + 1) & 1]);
       }
     }
     if (g.tma_store && lane == 0) bulk_wait<0>();
   } else if constexpr (kW4) {
     // ------------------------------------------------------------ nibble converters
-    const int ct = threadIdx.x - 32 * (2 + kEpiWarps);  // 0..127
+    const int ct = threadIdx.x - 32 * kEpiWarps;  // 0..127
     int s = 0;
     uint32_t ph = 0;
     for (int tile = tile0; tile < total_tiles; tile += tstride) {
@@ -427,12 +514,20 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     }
   }
 
+  if (g.probe != nullptr && lane == 0) {
+    // [cta][slot]: 0 tma empty-wait, 1 mma full-wait, 2 mma tempty-wait,
+    // 3 epi0 tfull-wait, 4 epi0 store-drain-wait, 5 total cycles (warp 0)
+    unsigned long long* pr = g.probe + blockIdx.x * 8;
+    if (warp == kTmaWarp) pr[0] = pw0;
+    if (warp == kMmaWarp) { pr[1] = pw0; pr[2] = pw1; }
+    if (warp == 0) { pr[3] = pw0; pr[4] = pw1; pr[5] = clock64() - t_start; }
+  }
   tc_fence_before();
   if constexpr (k2Cta)
     cluster_sync();
   else
     __syncthreads();
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     if constexpr (k2Cta)
       tmem_dealloc_cta2<kTmemCols>(tmem_base);

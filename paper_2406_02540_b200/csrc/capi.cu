@@ -119,13 +119,23 @@ int make_tmap_u8(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, i
 }
 
 // ------------------------------------------------------------------ FQ launch
-// (kernel instantiations live in fq_kernels.cu so they compile in parallel)
-int launch_fq(const dtq_fq::FqArgs& a, int x_dtype, bool exact, int cpt, bool vec, int block,
-              cudaStream_t st) {
-  int sms = device_info().sms;
-  cudaError_t e = dtq_launch_fq(a, x_dtype, exact, cpt, vec, block, sms, st);
+// (kernel instantiations live in fq_kernels.cu / fq_fast_*.cu)
+int fq_error(cudaError_t e) {
   if (e != cudaSuccess) return fail(DTQ_ERR_CUDA, "fused quantizer launch: %s", cudaGetErrorString(e));
   return DTQ_OK;
+}
+
+// fast-mode folded column multiplier: sign[c] / smooth[c] / sqrt(hblock)
+__global__ void col_mul_kernel(const double* __restrict__ smooth, const int8_t* __restrict__ signs,
+                               int hblock, int64_t K, float* __restrict__ out) {
+  const double norm = signs ? 1.0 / sqrt(static_cast<double>(hblock)) : 1.0;
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < K;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double m = norm;
+    if (smooth) m /= smooth[c];
+    if (signs && signs[c] < 0) m = -m;
+    out[c] = static_cast<float>(m);
+  }
 }
 
 size_t dtype_size(int dt) {
@@ -142,10 +152,23 @@ size_t dtype_size(int dt) {
   return 0;
 }
 
+// diagnostics: per-warp phase cycle counters of the fast quantizer, only when
+// DTQ_DEBUG_FQ_PROBE=1 (read back with dtq_diag_fq_probe_ptr)
+unsigned long long* fq_probe_buffer() {
+  static unsigned long long* p = [] {
+    const char* e = std::getenv("DTQ_DEBUG_FQ_PROBE");
+    unsigned long long* b = nullptr;
+    if (e && e[0] == '1' && cudaMalloc(&b, 65536 * 8 * 8) == cudaSuccess)
+      cudaMemset(b, 0, 65536 * 8 * 8);
+    return b;
+  }();
+  return p;
+}
+
 // Row quantizer; `smooth_mul` selects W * s (weight side) instead of X / s.
 int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx,
                        int bits, int symmetric, int mode, int smooth_mul, const double* smooth_d,
-                       const float* inv_smooth_f, const int8_t* signs, int hblock,
+                       const float* col_mul, const int8_t* signs, int hblock,
                        const dtq_prologue* pro, uint8_t* codes, int64_t ldc, double* scale,
                        int32_t* zero, int32_t* status, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: empty matrix");
@@ -173,19 +196,16 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
   DTQ_TRY(check_device());
 
   const bool exact = mode == DTQ_MODE_EXACT || x_dtype == DTQ_F64;
+  if (!exact && smooth_mul)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "weight-side smoothing runs in exact mode only");
+  if (!exact && (smooth_d || signs) && !col_mul)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "fast mode needs the folded column multiplier");
   const int64_t chunks = (cols + 7) / 8;
-  const int cpt = chunks <= 1024 ? 1 : 8;
-  const int64_t align = signs ? (hblock / 8 > 16 ? hblock / 8 : 16) : 16;
-  const int64_t tpr = round_up((chunks + cpt - 1) / cpt, align);
-  if (tpr > (cpt == 1 ? 1024 : 256))
-    return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: cols too large");
-  const int block = static_cast<int>(round_up(tpr, 32));
   const size_t es = dtype_size(x_dtype);
   const bool vec = cols % 8 == 0 && (ldx * es) % 16 == 0 &&
                    reinterpret_cast<uintptr_t>(x) % 16 == 0 && ldc % 8 == 0 &&
                    reinterpret_cast<uintptr_t>(codes) % 8 == 0 &&
                    (!smooth_d || reinterpret_cast<uintptr_t>(smooth_d) % 16 == 0) &&
-                   (!inv_smooth_f || reinterpret_cast<uintptr_t>(inv_smooth_f) % 16 == 0) &&
                    (kind == 0 || kind == 2 ||
                     (reinterpret_cast<uintptr_t>(pro->scale) % 16 == 0 &&
                      reinterpret_cast<uintptr_t>(pro->shift) % 16 == 0));
@@ -202,13 +222,7 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
   a.bits = bits;
   a.symmetric = symmetric;
   a.smooth_d = exact ? smooth_d : nullptr;
-  a.inv_smooth_f = exact ? nullptr : inv_smooth_f;
-  if (!exact && smooth_mul)
-    return fail(DTQ_ERR_INVALID_ARGUMENT, "weight-side smoothing runs in exact mode only");
-  if (exact && !smooth_d && inv_smooth_f)
-    return fail(DTQ_ERR_INVALID_ARGUMENT, "exact mode needs the fp64 smoothing vector");
-  if (!exact && smooth_d && !inv_smooth_f)
-    return fail(DTQ_ERR_INVALID_ARGUMENT, "fast mode needs the fp32 reciprocal smoothing vector");
+  a.col_mul = exact ? nullptr : col_mul;
   a.signs = signs;
   a.hblock = signs ? hblock : 0;
   a.pro_scale = pro ? pro->scale : nullptr;
@@ -217,9 +231,56 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
   a.status = status;
   a.pro = kind;
   a.smooth_mul = smooth_mul;
-  a.tpr = static_cast<int>(tpr);
+  a.probe = fq_probe_buffer();
+  const int sms = device_info().sms;
 
-  return launch_fq(a, x_dtype, exact, cpt, vec, block, st);
+  // the fp32 kernel needs 16-byte rows and a 128-column rotation block;
+  // anything else runs on the fp64 kernel (more precise, never less exact)
+  const bool fast = !exact && vec && (!signs || hblock == 128);
+  if (!fast) {
+    if (!exact && (smooth_d || signs) && !smooth_d && !signs) return DTQ_ERR_INVALID_ARGUMENT;
+    // CTA per row; 8-element chunks, 1 (K <= 8192) or 8 chunks per thread
+    const int cpt = chunks <= 1024 ? 1 : 8;
+    const int64_t align = signs ? (hblock / 8 > 16 ? hblock / 8 : 16) : 16;
+    const int64_t tpr = round_up((chunks + cpt - 1) / cpt, align);
+    if (tpr > (cpt == 1 ? 1024 : 256))
+      return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: cols too large");
+    a.tpr = static_cast<int>(tpr);
+    a.col_mul = nullptr;
+    if (!exact) {
+      // fp32 request on an unaligned / non-128-block input: exact kernel with
+      // the fp64 transforms it needs
+      if (smooth_d == nullptr && col_mul != nullptr && !signs)
+        return fail(DTQ_ERR_UNSUPPORTED, "unaligned fast-mode input needs the fp64 smoothing vector");
+      a.smooth_d = smooth_d;
+    }
+    return fq_error(dtq_launch_fq_exact(a, x_dtype, cpt, vec,
+                                        static_cast<int>(round_up(tpr, 32)), sms, st));
+  }
+  // fast: W warps per row group (W = 2 up to K = 2048, else 4), groups per CTA
+  // sized so the per-group smem (2 raw rows + fp32 row) leaves room for
+  // several CTAs per SM.  DTQ_FQ_WPR overrides W (diagnostics).
+  static const int forced_wpr = [] {
+    const char* e = std::getenv("DTQ_FQ_WPR");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int64_t steps = (chunks + 31) / 32;
+  const bool static_steps = steps <= 5;
+  int W = static_steps ? 1 : (cols <= 2048 ? 2 : 4);
+  if (forced_wpr == 1 || forced_wpr == 2 || forced_wpr == 4) W = forced_wpr;
+  const int64_t row_bytes = static_cast<int64_t>(dtq_fq::fq_fast_warp_bytes(cols, static_cast<int>(es)));
+  int gpc = static_cast<int>((56 * 1024) / row_bytes);
+  gpc = gpc < 1 ? 1 : gpc;
+  while (gpc * W > 8 && gpc > 1) --gpc;
+  const int block = 32 * W * gpc;
+  a.tpr = 32 * W;
+  const int cpt = (W == 1 && static_steps) ? static_cast<int>(steps) : 0;  // compile-time steps
+  const bool rot = signs != nullptr;
+  switch (x_dtype) {
+    case DTQ_F16: return fq_error(dtq_launch_fq_fast_f16(a, cpt, rot, block, sms, st));
+    case DTQ_BF16: return fq_error(dtq_launch_fq_fast_bf16(a, cpt, rot, block, sms, st));
+    default: return fq_error(dtq_launch_fq_fast_f32(a, cpt, rot, block, sms, st));
+  }
 }
 
 // ------------------------------------------------------------------ weight prep kernels
@@ -328,7 +389,7 @@ struct dtq_qlinear_s {
   double* bias = nullptr;     // [N] or null
   float* bias_f = nullptr;    // [N] or null
   double* smooth = nullptr;   // [K] or null
-  float* inv_smooth = nullptr;
+  float* col_mul = nullptr;     // [K] fast-mode folded sign / smooth / norm, or null
   int8_t* signs = nullptr;    // [K] or null
   int hblock = 0;
   CUtensorMap tmB[3];  // B operand boxes of 256, 128 and 64 rows
@@ -358,7 +419,7 @@ int grow(void** p, size_t* cur, size_t need) {
 
 void free_handle(dtq_qlinear_s* h) {
   void* ptrs[] = {h->w8, h->w4, h->s_w, h->s_w_f, h->wsum, h->bias, h->bias_f, h->smooth,
-                  h->inv_smooth, h->signs, h->scratch, h->acc32, h->hx, h->hy, h->status};
+                  h->col_mul, h->signs, h->scratch, h->acc32, h->hx, h->hy, h->status};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete h;
@@ -375,12 +436,8 @@ int copy_balance(dtq_qlinear_s* h, const dtq_balance* bal, cudaStream_t st) {
   const int64_t K = h->K;
   if (bal->smooth) {
     CUDA_TRY(cudaMalloc(&h->smooth, K * sizeof(double)));
-    CUDA_TRY(cudaMalloc(&h->inv_smooth, K * sizeof(float)));
     CUDA_TRY(cudaMemcpyAsync(h->smooth, bal->smooth, K * sizeof(double),
                              cudaMemcpyDeviceToDevice, st));
-    to_f32_kernel<<<static_cast<int>((K + 255) / 256), 256, 0, st>>>(h->smooth, h->inv_smooth,
-                                                                      K, 1);
-    CUDA_TRY(cudaGetLastError());
   }
   if (bal->signs) {
     if (bal->hblock < 8 || bal->hblock > 256 || (bal->hblock & (bal->hblock - 1)) != 0)
@@ -390,6 +447,12 @@ int copy_balance(dtq_qlinear_s* h, const dtq_balance* bal, cudaStream_t st) {
     CUDA_TRY(cudaMalloc(&h->signs, K));
     CUDA_TRY(cudaMemcpyAsync(h->signs, bal->signs, K, cudaMemcpyDeviceToDevice, st));
     h->hblock = bal->hblock;
+  }
+  if (h->smooth || h->signs) {
+    CUDA_TRY(cudaMalloc(&h->col_mul, K * sizeof(float)));
+    col_mul_kernel<<<static_cast<int>((K + 255) / 256), 256, 0, st>>>(h->smooth, h->signs,
+                                                                       h->hblock, K, h->col_mul);
+    CUDA_TRY(cudaGetLastError());
   }
   return DTQ_OK;
 }
@@ -610,7 +673,7 @@ int forward_impl(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear
   int32_t* z_x = reinterpret_cast<int32_t*>(base + off_z);
   DTQ_TRY(overflow_check(h->abits, h->wbits, h->K));
   DTQ_TRY(quantize_rows_impl(x, x_dtype, M, h->K, ldx, h->abits, 0, mode, 0, h->smooth,
-                             h->inv_smooth, h->signs, h->hblock, pro, codes, ldc, s_x, z_x,
+                             h->col_mul, h->signs, h->hblock, pro, codes, ldc, s_x, z_x,
                              status, st));
   return qgemm_impl(codes, ldc, s_x, z_x, M, h, y, y_dtype, ldy, st);
 }
@@ -628,28 +691,31 @@ int dtq_device_check(void) { return check_device(); }
 
 // diagnostics only (deliberately not declared in include/dtq_capi.h)
 void* dtq_diag_probe_ptr(void) { return probe_buffer(); }
+void* dtq_diag_fq_probe_ptr(void) { return fq_probe_buffer(); }
 
 int dtq_quantize_rows(const void* x, int x_dtype, int64_t rows, int64_t cols, int64_t ldx,
                       int bits, int symmetric, int mode, const dtq_balance* balance,
                       const dtq_prologue* prologue, uint8_t* codes, int64_t ldc, double* scale,
                       int32_t* zero, int32_t* status, void* stream) {
   const double* smooth = balance ? balance->smooth : nullptr;
+  const int8_t* signs = balance ? balance->signs : nullptr;
+  const int hblock = balance ? balance->hblock : 0;
   cudaStream_t st = as_stream(stream);
-  float* inv = nullptr;
+  float* mulv = nullptr;
   const bool exact = mode == DTQ_MODE_EXACT || x_dtype == DTQ_F64;
-  if (smooth && !exact) {
-    // fast mode multiplies by fp32 reciprocals: derive them stream-ordered
+  if ((smooth || signs) && !exact) {
+    // fast mode folds sign / smooth / norm into one fp32 multiplier: derive it
+    // stream-ordered for this call
     if (cols <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: empty matrix");
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&inv), cols * sizeof(float), st));
-    to_f32_kernel<<<static_cast<int>((cols + 255) / 256), 256, 0, st>>>(smooth, inv, cols, 1);
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&mulv), cols * sizeof(float), st));
+    col_mul_kernel<<<static_cast<int>((cols + 255) / 256), 256, 0, st>>>(smooth, signs, hblock,
+                                                                          cols, mulv);
     CUDA_TRY(cudaGetLastError());
   }
   const int r = quantize_rows_impl(x, x_dtype, rows, cols, ldx, bits, symmetric, mode, 0,
-                                   exact ? smooth : nullptr, inv,
-                                   balance ? balance->signs : nullptr,
-                                   balance ? balance->hblock : 0, prologue, codes, ldc, scale,
-                                   zero, status, st);
-  if (inv) cudaFreeAsync(inv, st);
+                                   exact ? smooth : nullptr, mulv, signs, hblock, prologue,
+                                   codes, ldc, scale, zero, status, st);
+  if (mulv) cudaFreeAsync(mulv, st);
   return r;
 }
 
@@ -819,7 +885,7 @@ int dtq_qlinear_quantize(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq
   if (!h) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: null handle");
   if (ldx < h->K) return fail(DTQ_ERR_INVALID_ARGUMENT, "qlinear_forward: X cols != C_in");
   return quantize_rows_impl(x, x_dtype, M, h->K, ldx, h->abits, 0, mode, 0, h->smooth,
-                            h->inv_smooth, h->signs, h->hblock, prologue, codes, ldc, scale, zero,
+                            h->col_mul, h->signs, h->hblock, prologue, codes, ldc, scale, zero,
                             status, as_stream(stream));
 }
 

@@ -1,14 +1,15 @@
-// fq_kernels.cu -- instantiations of the fused quantizer (fused_quant.cuh):
-// input {f16, bf16, f32, f64} x compute {fp32 "fast", fp64 "exact"} x
-// {1, 8} chunks per thread x {128-bit vector, scalar} loads.
+// fq_kernels.cu -- instantiations of the fp64 ("exact") fused quantizer
+// (fused_quant.cuh): input {f16, bf16, f32, f64} x {1, 8} chunks per thread
+// x {128-bit vector, scalar} loads.  The fp32 ("fast") kernels are in
+// fq_fast_*.cu.
 #include "../../include/dtq_capi.h"
 #include "launch.h"
 
 namespace {
 
-template <typename Tin, typename Tc, int kCPT, bool kVec>
-cudaError_t launch_fq_t(const dtq_fq::FqArgs& a, int block, int sms, cudaStream_t st) {
-  auto kern = dtq_fq::fq_kernel<Tin, Tc, kCPT, kVec>;
+template <typename Tin, int kCPT, bool kVec>
+cudaError_t launch_exact_t(const dtq_fq::FqArgs& a, int block, int sms, cudaStream_t st) {
+  auto kern = dtq_fq::fq_kernel<Tin, double, kCPT, kVec>;
   static thread_local int occ_cache[33] = {0};
   const int slot = block / 32;
   if (occ_cache[slot] == 0) {
@@ -23,31 +24,24 @@ cudaError_t launch_fq_t(const dtq_fq::FqArgs& a, int block, int sms, cudaStream_
   return cudaGetLastError();
 }
 
-template <typename Tin, typename Tc>
-cudaError_t launch_fq_c(const dtq_fq::FqArgs& a, int cpt, bool vec, int block, int sms,
-                        cudaStream_t st) {
+template <typename Tin>
+cudaError_t launch_exact_c(const dtq_fq::FqArgs& a, int cpt, bool vec, int block, int sms,
+                           cudaStream_t st) {
   if (cpt == 1)
-    return vec ? launch_fq_t<Tin, Tc, 1, true>(a, block, sms, st)
-               : launch_fq_t<Tin, Tc, 1, false>(a, block, sms, st);
-  return vec ? launch_fq_t<Tin, Tc, 8, true>(a, block, sms, st)
-             : launch_fq_t<Tin, Tc, 8, false>(a, block, sms, st);
+    return vec ? launch_exact_t<Tin, 1, true>(a, block, sms, st)
+               : launch_exact_t<Tin, 1, false>(a, block, sms, st);
+  return vec ? launch_exact_t<Tin, 8, true>(a, block, sms, st)
+             : launch_exact_t<Tin, 8, false>(a, block, sms, st);
 }
 
 }  // namespace
 
-cudaError_t dtq_launch_fq(const dtq_fq::FqArgs& a, int x_dtype, bool exact, int cpt, bool vec,
-                          int block, int sms, cudaStream_t st) {
-  if (exact) {
-    switch (x_dtype) {
-      case DTQ_F16: return launch_fq_c<__half, double>(a, cpt, vec, block, sms, st);
-      case DTQ_BF16: return launch_fq_c<__nv_bfloat16, double>(a, cpt, vec, block, sms, st);
-      case DTQ_F32: return launch_fq_c<float, double>(a, cpt, vec, block, sms, st);
-      default: return launch_fq_c<double, double>(a, cpt, vec, block, sms, st);
-    }
-  }
+cudaError_t dtq_launch_fq_exact(const dtq_fq::FqArgs& a, int x_dtype, int cpt, bool vec,
+                                int block, int sms, cudaStream_t st) {
   switch (x_dtype) {
-    case DTQ_F16: return launch_fq_c<__half, float>(a, cpt, vec, block, sms, st);
-    case DTQ_BF16: return launch_fq_c<__nv_bfloat16, float>(a, cpt, vec, block, sms, st);
-    default: return launch_fq_c<float, float>(a, cpt, vec, block, sms, st);
+    case DTQ_F16: return launch_exact_c<__half>(a, cpt, vec, block, sms, st);
+    case DTQ_BF16: return launch_exact_c<__nv_bfloat16>(a, cpt, vec, block, sms, st);
+    case DTQ_F32: return launch_exact_c<float>(a, cpt, vec, block, sms, st);
+    default: return launch_exact_c<double>(a, cpt, vec, block, sms, st);
   }
 }

@@ -59,6 +59,8 @@ struct FqArgs {
   int32_t* status;            // nullable; |= 1 on non-finite input
   int pro;                    // Prologue
   int smooth_mul;             // 1: W * s (weight side of apply_scaling)
+  const float* col_mul;       // fast kernel: folded sign/s_c/sqrt(hblock) per column
+  unsigned long long* probe;  // diagnostics: per-warp phase cycles (or nullptr)
   int tpr;                    // threads per row (multiple of 16 and of hblock/8)
 };
 

@@ -6,11 +6,19 @@
 #include <cuda_runtime.h>
 
 #include "fused_quant.cuh"
+#include "fused_quant_fast.cuh"
 #include "qgemm_sm100.cuh"
 
-// fused activation / weight quantizer; x_dtype is a dtq_dtype
-cudaError_t dtq_launch_fq(const dtq_fq::FqArgs& a, int x_dtype, bool exact, int cpt, bool vec,
-                          int block, int sms, cudaStream_t st);
+// fused activation / weight quantizer: fp64 "exact" kernel (x_dtype is a
+// dtq_dtype) and the fp32 "fast" kernels per input type
+cudaError_t dtq_launch_fq_exact(const dtq_fq::FqArgs& a, int x_dtype, int cpt, bool vec,
+                                int block, int sms, cudaStream_t st);
+cudaError_t dtq_launch_fq_fast_f16(const dtq_fq::FqArgs& a, int cpt, bool rot, int block, int sms,
+                                   cudaStream_t st);
+cudaError_t dtq_launch_fq_fast_bf16(const dtq_fq::FqArgs& a, int cpt, bool rot, int block, int sms,
+                                    cudaStream_t st);
+cudaError_t dtq_launch_fq_fast_f32(const dtq_fq::FqArgs& a, int cpt, bool rot, int block, int sms,
+                                   cudaStream_t st);
 
 // tcgen05 integer GEMM tile configurations
 struct GemmCfg {

@@ -227,6 +227,107 @@ def run_reference(args, world, rank):
     print(json.dumps(out), flush=True)
 
 
+# ---------------------------------------------------------------------- block stack
+# PixArt-alpha (hidden 1152, MLP x4) block linears at batch 4, 1024 px:
+# 4 x 64 x 64 = 16384 image tokens, 4 x 120 = 480 T5 text tokens.
+# (name, K, N, rows, prologue) -- prologue fused into the quantizer:
+#   ln_mod  LayerNorm + adaLN modulate (t2i_modulate) in front of qkv / fc1
+#   gelu    GELU on the fc1 output in front of fc2
+STACK_LAYERS = [("attn.qkv", 1152, 3456, "img", "ln_mod"), ("attn.proj", 1152, 1152, "img", None),
+                ("cross.q", 1152, 1152, "img", None), ("cross.kv", 1152, 2304, "txt", None),
+                ("cross.proj", 1152, 1152, "img", None), ("mlp.fc1", 1152, 4608, "img", "ln_mod"),
+                ("mlp.fc2", 4608, 1152, "img", "gelu")]
+STACK_BLOCKS, STACK_IMG, STACK_TXT = 28, 16384, 480
+
+
+def stack_ops(blocks=STACK_BLOCKS):
+    rows = {"img": STACK_IMG, "txt": STACK_TXT}
+    return blocks * sum(2.0 * rows[r] * k * n for _, k, n, r, _ in STACK_LAYERS)
+
+
+def run_stack(dev, reps: int = 10):
+    """28-block PixArt-alpha linear stack: W8A8 (smooth + 128-block Hadamard
+    fused into every quantizer, adaLN / GELU prologues fused) vs FP16 cuBLAS
+    (torch.matmul, plus the same LayerNorm / modulate / GELU elementwise ops
+    for the prologue-bearing layers).  Both captured in CUDA graphs; weights
+    random-init, activations synthetic; one forward = 196 linears."""
+    import torch
+    import torch.nn.functional as F
+    import paper_2406_02540_b200 as dtq
+
+    g = torch.Generator(device=dev).manual_seed(7)
+    rows = {"img": STACK_IMG, "txt": STACK_TXT}
+    xin = {k: (torch.randn((rows[r], k), generator=g, device=dev) * 2).half()
+           for _, k, _, r, _ in STACK_LAYERS for k in [k]}
+    xin_txt = (torch.randn((STACK_TXT, 1152), generator=g, device=dev)).half()
+    sc = torch.randn(1152, generator=g, device=dev) * 0.1
+    sh = torch.randn(1152, generator=g, device=dev) * 0.1
+    signs = torch.from_numpy(dtq.hadamard_signs(4608, 7)).to(dev)
+    layers, wts, outs = [], [], {}
+    for b in range(STACK_BLOCKS):
+        for name, k, n, r, pro in STACK_LAYERS:
+            w = (torch.randn((n, k), generator=g, device=dev) / k ** 0.5).half()
+            smooth = (torch.rand(k, generator=g, device=dev, dtype=torch.float64) + 0.5)
+            bal = dtq.Balance(smooth, signs[:k].contiguous(), 128)
+            layers.append((dtq.QuantLinear.create(w, 8, 8, balance=bal), r, k, n, pro))
+            wts.append((w, r, k, n, pro))
+    for _, k, n, r, _ in STACK_LAYERS:
+        outs[(r, n)] = torch.empty((rows[r], n), dtype=torch.float16, device=dev)
+    ws = torch.empty(max(l.workspace(STACK_IMG, dev).numel() for l, *_ in layers[:7]),
+                     dtype=torch.uint8, device=dev)
+    pro_ln = dtq.Prologue(dtq.PROLOGUE_LN_MODULATE, sc, sh, 1e-6)
+    pro_gelu = dtq.Prologue(dtq.PROLOGUE_GELU)
+
+    def ours():
+        for layer, r, k, n, pro in layers:
+            x = xin_txt if r == "txt" else xin[k]
+            p = pro_ln if pro == "ln_mod" else (pro_gelu if pro == "gelu" else None)
+            layer.forward(x, out=outs[(r, n)], prologue=p, workspace=ws)
+
+    def fp16():
+        for w, r, k, n, pro in wts:
+            x = xin_txt if r == "txt" else xin[k]
+            if pro == "ln_mod":
+                x = F.layer_norm(x, (k,), eps=1e-6) * (1 + sc.half()) + sh.half()
+            elif pro == "gelu":
+                x = F.gelu(x)
+            torch.matmul(x, w.t(), out=outs[(r, n)])
+
+    def fp16_gemm_only():
+        for w, r, k, n, pro in wts:
+            x = xin_txt if r == "txt" else xin[k]
+            torch.matmul(x, w.t(), out=outs[(r, n)])
+
+    res = {}
+    for key, fn in (("w8a8", ours), ("fp16_cublas", fp16), ("fp16_cublas_gemm_only", fp16_gemm_only)):
+        fn()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            fn()
+        graph.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            graph.replay()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        res[key] = float(np.median(ts))
+        del graph
+    ops = stack_ops()
+    return {"workload": "PixArt-alpha 28-block linear stack, batch 4, 1024px "
+                        "(16384 image + 480 text tokens), 196 linears/forward, CUDA graphs",
+            "ms": res["w8a8"], "tops": ops / (res["w8a8"] * 1e-3) / 1e12,
+            "fp16_cublas_ms": res["fp16_cublas"],
+            "fp16_cublas_gemm_only_ms": res["fp16_cublas_gemm_only"],
+            "speedup_vs_fp16": res["fp16_cublas"] / res["w8a8"],
+            "speedup_vs_fp16_gemm_only": res["fp16_cublas_gemm_only"] / res["w8a8"],
+            "ops": ops}
+
+
 # ---------------------------------------------------------------------- GPU arm
 def run_ours(args, world, rank, local):
     import torch
@@ -341,6 +442,12 @@ def run_ours(args, world, rank, local):
     except Exception:
         t_i8 = None
 
+    stack = None
+    if not args.no_stack:
+        try:
+            stack = run_stack(dev)
+        except Exception as e:  # reported, never silently replaced
+            stack = {"error": repr(e)[:200]}
     if rank != 0:
         return
     hbm, bf16, peak_src = load_peaks()
@@ -395,6 +502,7 @@ def run_ours(args, world, rank, local):
         "e2e": {"value": ops * world / t_e2e / 1e12, "unit": "TOPS",
                 "h2d_bytes_per_step": 2 * M * K, "d2h_bytes_per_step": 2 * M * N,
                 "ms": t_e2e * 1e3, "api": "dtq_qlinear_forward_host"},
+        "stack": stack,
         "gpu_launches": 2 * args.steps,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
@@ -410,6 +518,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-rows", type=int, default=512)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-stack", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -234,9 +234,10 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
   a.probe = fq_probe_buffer();
   const int sms = device_info().sms;
 
-  // the fp32 kernel needs 16-byte rows and a 128-column rotation block;
-  // anything else runs on the fp64 kernel (more precise, never less exact)
-  const bool fast = !exact && vec && (!signs || hblock == 128);
+  // the fp32 kernel needs 16-byte rows, K % 128 == 0 and a 128-column
+  // rotation block; anything else runs on the fp64 kernel (more precise,
+  // never less exact)
+  const bool fast = !exact && vec && cols % 128 == 0 && (!signs || hblock == 128);
   if (!fast) {
     if (!exact && (smooth_d || signs) && !smooth_d && !signs) return DTQ_ERR_INVALID_ARGUMENT;
     // CTA per row; 8-element chunks, 1 (K <= 8192) or 8 chunks per thread
@@ -257,24 +258,22 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
     return fq_error(dtq_launch_fq_exact(a, x_dtype, cpt, vec,
                                         static_cast<int>(round_up(tpr, 32)), sms, st));
   }
-  // fast: W warps per row group (W = 2 up to K = 2048, else 4), groups per CTA
-  // sized so the per-group smem (2 raw rows + fp32 row) leaves room for
-  // several CTAs per SM.  DTQ_FQ_WPR overrides W (diagnostics).
-  static const int forced_wpr = [] {
-    const char* e = std::getenv("DTQ_FQ_WPR");
+  // fast: G 8-lane groups per row, R = 4/G rows per warp with R*K <= 4608
+  // (18 KB fp32 park buffer per warp); warps per CTA sized for ~2 CTAs/SM
+  int G = 2;
+  while (G < 4 && (4 / G) * cols > 2304) G *= 2;
+  static const int forced_g = [] {
+    const char* e = std::getenv("DTQ_FQ_G");
     return e ? std::atoi(e) : 0;
   }();
-  const int64_t steps = (chunks + 31) / 32;
-  const bool static_steps = steps <= 5;
-  int W = static_steps ? 1 : (cols <= 2048 ? 2 : 4);
-  if (forced_wpr == 1 || forced_wpr == 2 || forced_wpr == 4) W = forced_wpr;
-  const int64_t row_bytes = static_cast<int64_t>(dtq_fq::fq_fast_warp_bytes(cols, static_cast<int>(es)));
-  int gpc = static_cast<int>((56 * 1024) / row_bytes);
-  gpc = gpc < 1 ? 1 : gpc;
-  while (gpc * W > 8 && gpc > 1) --gpc;
-  const int block = 32 * W * gpc;
-  a.tpr = 32 * W;
-  const int cpt = (W == 1 && static_steps) ? static_cast<int>(steps) : 0;  // compile-time steps
+  if (forced_g == 1 || forced_g == 2 || forced_g == 4) G = forced_g;
+  const size_t wbytes = dtq_fq::fq_fast_warp_bytes(cols, G, static_cast<int>(es));
+  int wpc = static_cast<int>((113 * 1024) / wbytes);
+  wpc = wpc < 1 ? 1 : (wpc > 8 ? 8 : wpc);
+  if (wbytes * wpc > 227 * 1024) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: cols too large");
+  const int block = 32 * wpc;
+  a.tpr = 32;
+  const int cpt = G;
   const bool rot = signs != nullptr;
   switch (x_dtype) {
     case DTQ_F16: return fq_error(dtq_launch_fq_fast_f16(a, cpt, rot, block, sms, st));

@@ -1,16 +1,15 @@
 // fq_fast_bf16.cu -- fp32 fused-quantizer instantiations for __nv_bfloat16 input
-// (fused_quant_fast.cuh): without / with the 128-column rotation, for the
-// compile-time step counts up to 5 (K <= 1280, e.g. the 1152-wide STDiT /
-// PixArt activations) and a runtime-step, multi-warp-per-row fallback.
+// (fused_quant_fast.cuh): without / with the 128-column rotation, for
+// G = 1, 2, 4 lane groups (of 8 lanes) per row.
 #include "launch.h"
 
 namespace {
 
-template <bool kRot, int kNit>
+template <bool kRot, int G, int kNblk>
 cudaError_t launch_t(const dtq_fq::FqArgs& a, int block, int sms, cudaStream_t st) {
-  auto kern = dtq_fq::fq_fast_kernel<__nv_bfloat16, kRot, kNit>;
-  const int rows_per_cta = block / a.tpr;
-  const size_t smem = dtq_fq::fq_fast_smem_bytes(rows_per_cta, a.K, 2);
+  auto kern = dtq_fq::fq_fast_kernel<__nv_bfloat16, kRot, G, kNblk>;
+  const int warps = block / 32;
+  const size_t smem = warps * dtq_fq::fq_fast_warp_bytes(a.K, G, 2);
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(smem));
@@ -19,6 +18,7 @@ cudaError_t launch_t(const dtq_fq::FqArgs& a, int block, int sms, cudaStream_t s
   int occ = 0;
   const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem);
   if (e != cudaSuccess) return e;
+  const int rows_per_cta = warps * (4 / G);
   const int64_t ctas = (a.M + rows_per_cta - 1) / rows_per_cta;
   const int64_t cap = static_cast<int64_t>(sms) * (occ > 0 ? occ : 1);
   const int grid = static_cast<int>(ctas < cap ? ctas : cap);
@@ -26,22 +26,26 @@ cudaError_t launch_t(const dtq_fq::FqArgs& a, int block, int sms, cudaStream_t s
   return cudaGetLastError();
 }
 
+template <bool kRot, int G>
+cudaError_t launch_k(const dtq_fq::FqArgs& a, int block, int sms, cudaStream_t st) {
+  // (compile-time-K instantiations measured slower: full unrolling bloats
+  // the code; the runtime-K loop is used for every width)
+  return launch_t<kRot, G, 0>(a, block, sms, st);
+}
+
 template <bool kRot>
-cudaError_t launch_r(const dtq_fq::FqArgs& a, int nit, int block, int sms, cudaStream_t st) {
-  switch (nit) {
-    case 1: return launch_t<kRot, 1>(a, block, sms, st);
-    case 2: return launch_t<kRot, 2>(a, block, sms, st);
-    case 3: return launch_t<kRot, 3>(a, block, sms, st);
-    case 4: return launch_t<kRot, 4>(a, block, sms, st);
-    case 5: return launch_t<kRot, 5>(a, block, sms, st);
-    default: return launch_t<kRot, 0>(a, block, sms, st);
+cudaError_t launch_r(const dtq_fq::FqArgs& a, int G, int block, int sms, cudaStream_t st) {
+  switch (G) {
+    case 1: return launch_k<kRot, 1>(a, block, sms, st);
+    case 2: return launch_k<kRot, 2>(a, block, sms, st);
+    default: return launch_k<kRot, 4>(a, block, sms, st);
   }
 }
 
 }  // namespace
 
-// nit: compile-time step count to use (0 = runtime loop with tpr/32 warps per row)
-cudaError_t dtq_launch_fq_fast_bf16(const dtq_fq::FqArgs& a, int nit, bool rot, int block,
+// G: 8-lane groups per row (1, 2 or 4)
+cudaError_t dtq_launch_fq_fast_bf16(const dtq_fq::FqArgs& a, int G, bool rot, int block,
                                   int sms, cudaStream_t st) {
-  return rot ? launch_r<true>(a, nit, block, sms, st) : launch_r<false>(a, nit, block, sms, st);
+  return rot ? launch_r<true>(a, G, block, sms, st) : launch_r<false>(a, G, block, sms, st);
 }

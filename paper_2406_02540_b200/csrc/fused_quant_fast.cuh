@@ -1,28 +1,37 @@
 // fused_quant_fast.cuh -- fp32 ("fast") fused quantizer.
 //
 // Same contract as fq_kernel (fused_quant.cuh) with fp32 transforms, built
-// for throughput on a memory-bound op:
-//   * one warp per token row, any K.  The whole input row arrives by one
-//     bulk async copy (cp.async.bulk, mbarrier-completed) into a per-warp
-//     double buffer, issued one row AHEAD, so HBM latency overlaps the
-//     previous row's arithmetic; the row is then walked in 256-column steps
-//     from shared memory and the transformed fp32 values parked in a per-warp
-//     row buffer: registers stay low and the loop body is small;
-//   * sign flip, smoothing (1/s_c) and the 1/sqrt(128) normalisation are one
-//     folded per-column multiplier (col_mul, L1-resident) applied before the
-//     butterflies (linearity; differs from the fp64 reference only by
-//     rounding, covered by the 1-LSB parity bar);
-//   * 128-column Walsh-Hadamard butterflies: strides 1/2/4 in registers
-//     (packed FADD2), strides 8..64 via __shfl_xor within 16-lane groups;
-//   * codes: q = v*(1/s)+z in one FFMA2, rounding by the 1.5*2^23 add whose
-//     low byte is the code; |frac - 1/2| < 2^-14 (the fp32 error bound) is
-//     recomputed with an IEEE fp64 divide (rare); the clamp is skipped on
-//     rows whose min-max params already bound q (the bounds themselves are
-//     near-ties and take the exact path).
-// With no prologue, smoothing or rotation the codes, s and z are
-// bit-identical to the reference (quant.cpp:90-113, 169-175).
-// Host contract: K % 8 == 0, 16-byte aligned rows, rotation block 128,
-// dynamic smem = fq_fast_smem_bytes(warps_per_cta, K, sizeof(Tin)).
+// for throughput on a memory-bound op.
+//
+// Work decomposition.  A 128-column block of a row is owned by an 8-lane
+// group, 16 consecutive columns per lane (two 128-bit loads, one 128-bit
+// code store).  A warp = 4 lane groups; G = 1, 2 or 4 groups cooperate on a
+// row, so one warp holds R = 4/G rows at once and walks their blocks in
+// nblocks/G steps.  Consequences:
+//   * the 128-point Walsh-Hadamard transform needs 4 in-register stages
+//     (strides 1..8, three of them packed FADD2/FFMA2) and only 3 shuffle
+//     stages (strides 16, 32, 64 = lane xor 1, 2, 4);
+//   * the fp64 parameter math (quant.cpp:90-113) runs once per warp for R
+//     rows at a time;
+//   * row min/max = 3 + log2(G) shuffle levels, no barriers.
+// Input rows arrive by one bulk async copy per row (cp.async.bulk,
+// mbarrier-completed) into shared memory; the next row group is fetched as
+// soon as pass 1 has consumed the current one, overlapping the parameter
+// math and the code pass.  Transformed values are parked in a per-warp fp32
+// row buffer between the min/max pass and the code pass.
+//
+// Arithmetic.  Sign flip, smoothing (1/s_c) and 1/sqrt(128) are ONE folded
+// per-column multiplier (col_mul) applied before the butterflies (linearity;
+// differs from the fp64 reference only by rounding, within the 1-LSB parity
+// bar).  Codes: q = v*(1/s)+z in one FFMA2, rounding by the 1.5*2^23 add
+// whose low byte is the code; |frac - 1/2| < 2^-14 (the fp32 error bound)
+// is recomputed with an IEEE fp64 divide (rare); the clamp is skipped on rows
+// whose min-max params already bound q (those bounds are near-ties and take
+// the exact path).  With no prologue, smoothing or rotation the codes, s and
+// z are bit-identical to the reference (quant.cpp:90-113, 169-175).
+//
+// Host contract: K % 128 == 0, 16-byte aligned rows, rotation block 128,
+// blockDim = 32 * warps, dynamic smem = warps * fq_fast_warp_bytes(K, G, in).
 #pragma once
 
 #include "fused_quant.cuh"
@@ -35,193 +44,201 @@ __device__ __forceinline__ float2 f2sub(float2 a, float2 b) {
   return __ffma2_rn(b, make_float2(-1.f, -1.f), a);
 }
 
-// per warp: 2 raw input rows (K * sizeof(Tin), 128-byte padded), the fp32 row
-// buffer (ceil(K/256) KB) and 2 mbarriers
-__host__ __device__ constexpr size_t fq_fast_warp_bytes(int64_t K, int in_bytes) {
-  return 2 * ((static_cast<size_t>(K) * in_bytes + 127) / 128 * 128) +
-         static_cast<size_t>((K + 255) / 256) * 1024 + 16;
-}
-__host__ __device__ constexpr size_t fq_fast_smem_bytes(int warps, int64_t K, int in_bytes) {
-  return static_cast<size_t>(warps) * fq_fast_warp_bytes(K, in_bytes);
+// per warp: R = 4/G raw input rows + R fp32 rows + 1 mbarrier
+__host__ __device__ constexpr size_t fq_fast_warp_bytes(int64_t K, int G, int in_bytes) {
+  return static_cast<size_t>(4 / G) * static_cast<size_t>(K) * (in_bytes + 4) + 16;
 }
 
 template <typename Tin>
-__device__ __forceinline__ void load8(const Tin* p, bool ok, float (&v)[8]) {  // shared memory
-  uint4 r[Vec<Tin>::kWords];
+__device__ __forceinline__ void load16(const Tin* p, float (&v)[16]) {  // shared memory
+  uint4 r0[Vec<Tin>::kWords], r1[Vec<Tin>::kWords];
 #pragma unroll
-  for (int w = 0; w < Vec<Tin>::kWords; ++w)
-    r[w] = ok ? reinterpret_cast<const uint4*>(p)[w] : make_uint4(0u, 0u, 0u, 0u);
-  unpack<float>(r, v, Tin());
+  for (int w = 0; w < Vec<Tin>::kWords; ++w) {
+    r0[w] = reinterpret_cast<const uint4*>(p)[w];
+    r1[w] = reinterpret_cast<const uint4*>(p + 8)[w];
+  }
+  float a[8], b[8];
+  unpack<float>(r0, a, Tin());
+  unpack<float>(r1, b, Tin());
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    v[e] = a[e];
+    v[e + 8] = b[e];
+  }
 }
 
-// kNit > 0: the row has exactly kNit 256-column steps (compile-time; one warp
-// per row, fully unrolled, only the last step can be partial); kNit == 0:
-// runtime step count, W = tpr/32 warps per row.
-template <typename Tin, bool kRot, int kNit>
+// kNblk > 0: compile-time K = 128 * kNblk (static steps, offsets and
+// predicates); kNblk == 0: runtime K.
+template <typename Tin, bool kRot, int G, int kNblk>
 __global__ void __launch_bounds__(256) fq_fast_kernel(const FqArgs a) {
+  constexpr int R = 4 / G;  // rows per warp
   extern __shared__ __align__(128) uint8_t fq_smem[];
   const int lane = threadIdx.x & 31;
-  const int W = kNit > 0 ? 1 : (a.tpr >> 5);  // warps per row group
-  const int g = (threadIdx.x >> 5) / W;      // row group in the CTA
-  const int wg = (threadIdx.x >> 5) - g * W; // warp within the group
-  const int groups = (blockDim.x >> 5) / W;
-  const int K = static_cast<int>(a.K);
-  const int chunks = K >> 3;
-  const int nit = kNit > 0 ? kNit : (chunks + 31) >> 5;  // 256-column steps (step i -> warp i % W)
-  const uint32_t row_in = static_cast<uint32_t>(K) * sizeof(Tin);
-  const size_t raw_pitch = (static_cast<size_t>(row_in) + 127) / 128 * 128;
-  uint8_t* wbase = fq_smem + g * fq_fast_warp_bytes(K, sizeof(Tin));
-  uint8_t* const raw0 = wbase;
-  uint8_t* const raw1 = wbase + raw_pitch;
-  float* buf = reinterpret_cast<float*>(wbase + 2 * raw_pitch);  // [step][half][lane][4]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wbase + 2 * raw_pitch + nit * 1024);
-  __shared__ float red[8][4][2];  // [group][warp][min, max]
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int lg = lane >> 3;  // lane group 0..3
+  const int li = lane & 7;   // lane within the group
+  const int rl = lg / G;     // local row of this lane group
+  const int gi = lg % G;     // group index within the row
+  const int K = kNblk > 0 ? 128 * kNblk : static_cast<int>(a.K);
+  const int nblk = K >> 7;
+  const int steps = (nblk + G - 1) / G;
+  // block st*G+gi is valid for every lane group except possibly in the last step
+  auto blk_ok = [&](int st, int blk) -> bool {
+    return (kNblk > 0 && (st + 1) * G <= kNblk) || blk < nblk;
+  };
+  uint8_t* wbase = fq_smem + warp * fq_fast_warp_bytes(K, G, sizeof(Tin));
+  const Tin* raw = reinterpret_cast<const Tin*>(wbase);  // [R][K]
+  float* park = reinterpret_cast<float*>(wbase + static_cast<size_t>(R) * K * sizeof(Tin));
+  uint64_t* bar =
+      reinterpret_cast<uint64_t*>(wbase + static_cast<size_t>(R) * K * (sizeof(Tin) + 4));
   const Tin* __restrict__ X = static_cast<const Tin*>(a.x);
   const int qmax_i = (1 << a.bits) - 1;
-  const float sg_1 = (lane & 1) ? -1.f : 1.f, sg_2 = (lane & 2) ? -1.f : 1.f;
-  const float sg_4 = (lane & 4) ? -1.f : 1.f, sg_8 = (lane & 8) ? -1.f : 1.f;
-  const bool leader = wg == 0 && lane == 0;  // issues the group's row copies
-  auto group_sync = [&]() {
-    if (W > 1)
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(32 * W) : "memory");
-    else
-      __syncwarp();
-  };
+  const uint32_t row_in = static_cast<uint32_t>(K) * sizeof(Tin);
+  const float sgn1 = (li & 1) ? -1.f : 1.f, sgn2 = (li & 2) ? -1.f : 1.f;
+  const float sgn4 = (li & 4) ? -1.f : 1.f;
 
-  if (leader) {
-    dtq_ptx::mbar_init(&bar[0], 1);
-    dtq_ptx::mbar_init(&bar[1], 1);
+  if (lane == 0) {
+    dtq_ptx::mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-  const int64_t rstep = static_cast<int64_t>(gridDim.x) * groups;
-  auto issue = [&](int64_t r, int b) {  // leader: bulk copy of row r into raw[b]
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of raw[b]
-    dtq_ptx::mbar_arrive_expect_tx(&bar[b], row_in);
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            dtq_ptx::smem_u32(b ? raw1 : raw0)),
-        "l"(reinterpret_cast<uint64_t>(X + r * a.ldx)), "r"(row_in), "r"(dtq_ptx::smem_u32(&bar[b]))
-        : "memory");
+  __syncwarp();
+  const int64_t gstride = static_cast<int64_t>(gridDim.x) * nwarps * R;
+  // lane 0 fetches the R rows of a group (rows past M are skipped)
+  auto issue = [&](int64_t g0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    int n = 0;
+    for (int r = 0; r < R; ++r) n += (g0 + r < a.M) ? 1 : 0;
+    dtq_ptx::mbar_arrive_expect_tx(bar, row_in * n);
+    for (int r = 0; r < n; ++r)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+          "[%3];" ::"r"(dtq_ptx::smem_u32(raw + static_cast<size_t>(r) * K)),
+          "l"(reinterpret_cast<uint64_t>(X + (g0 + r) * a.ldx)), "r"(row_in),
+          "r"(dtq_ptx::smem_u32(bar))
+          : "memory");
   };
-  int64_t row = static_cast<int64_t>(blockIdx.x) * groups + g;
-  if (leader && row < a.M) issue(row, 0);
-  uint32_t phase = 0u;  // bit b = parity of bar[b]
+  int64_t r0 = (static_cast<int64_t>(blockIdx.x) * nwarps + warp) * R;
+  if (lane == 0 && r0 < a.M) issue(r0);
+  uint32_t phase = 0;
 
-  for (int it = 0; row < a.M; row += rstep, ++it) {
-    const int b = it & 1;
-    if (leader && row + rstep < a.M) issue(row + rstep, b ^ 1);  // next row, in flight now
-    long long tp0 = a.probe ? clock64() : 0;
-    dtq_ptx::mbar_wait(&bar[b], (phase >> b) & 1u);
-    long long tp1 = a.probe ? clock64() : 0;
-    phase ^= 1u << b;
-    const Tin* xr = reinterpret_cast<const Tin*>(b ? raw1 : raw0);  // this row, in smem
+  for (; r0 < a.M; r0 += gstride) {
+    const int64_t row = r0 + rl;
+    const bool row_ok = row < a.M;
+    dtq_ptx::mbar_wait(bar, phase);
+    phase ^= 1u;
+    const Tin* xr = raw + static_cast<size_t>(rl) * K;
+    float* pr = park + static_cast<size_t>(rl) * K;  // [block][quarter][lane][4]
 
-    // ---- optional LayerNorm statistics (extra pass over the row, L1/L2 hits)
+    // ---- optional LayerNorm statistics (reads the row from smem)
     float mean = 0.f, rstd = 1.f;
     if (a.pro == kProLnModulate) {
       float s1 = 0.f, s2 = 0.f;
-#pragma unroll(kNit > 0 ? kNit : 1)
-      for (int i = wg; i < nit; i += W) {
-        const int c = i * 32 + lane;
-        float v[8];
-        load8<Tin>(xr + c * 8, (kNit > 0 && i < kNit - 1) || c < chunks, v);
+      for (int st = 0; st < steps; ++st) {
+        const int blk = st * G + gi;
+        if (row_ok && blk < nblk) {
+          float v[16];
+          load16<Tin>(xr + blk * 128 + li * 16, v);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) s1 += v[e];
+          for (int e = 0; e < 16; ++e) s1 += v[e];
+        }
       }
 #pragma unroll
-      for (int m = 16; m >= 1; m >>= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, m);
-      if (W > 1) {
-        if (lane == 0) red[g][wg][0] = s1;
-        group_sync();
-        s1 = 0.f;
-        for (int w = 0; w < W; ++w) s1 += red[g][w][0];
-        group_sync();
-      }
+      for (int m = 1; m < 8 * G; m <<= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, m);
       mean = s1 / static_cast<float>(K);
-#pragma unroll(kNit > 0 ? kNit : 1)
-      for (int i = wg; i < nit; i += W) {
-        const int c = i * 32 + lane;
-        const bool ok = (kNit > 0 && i < kNit - 1) || c < chunks;
-        float v[8];
-        load8<Tin>(xr + c * 8, ok, v);
+      for (int st = 0; st < steps; ++st) {
+        const int blk = st * G + gi;
+        if (row_ok && blk < nblk) {
+          float v[16];
+          load16<Tin>(xr + blk * 128 + li * 16, v);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) s2 += ok ? (v[e] - mean) * (v[e] - mean) : 0.f;
+          for (int e = 0; e < 16; ++e) s2 += (v[e] - mean) * (v[e] - mean);
+        }
       }
 #pragma unroll
-      for (int m = 16; m >= 1; m >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, m);
-      if (W > 1) {
-        if (lane == 0) red[g][wg][0] = s2;
-        group_sync();
-        s2 = 0.f;
-        for (int w = 0; w < W; ++w) s2 += red[g][w][0];
-        group_sync();
-      }
+      for (int m = 1; m < 8 * G; m <<= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, m);
       rstd = rsqrtf(s2 / static_cast<float>(K) + a.eps);
     }
 
-    // ---- pass 1: load, prologue, multiplier, butterflies, min / max -> smem
+    // ---- pass 1: prologue, multiplier, butterflies, min / max; park in smem
     float mn = __int_as_float(0x7f800000), mx = -mn;
     bool bad = false;
-#pragma unroll(kNit > 0 ? kNit : 1)
-    for (int i = wg; i < nit; i += W) {
-      const int c = i * 32 + lane;
-      const bool ok = (kNit > 0 && i < kNit - 1) || c < chunks;
-      float v[8];
-      load8<Tin>(xr + c * 8, ok, v);
+#pragma unroll(kNblk > 0 ? (kNblk + G - 1) / G : 1)
+    for (int st = 0; st < steps; ++st) {
+      const int blk = st * G + gi;
+      const bool ok = row_ok && blk_ok(st, blk);
+      const int c0 = (ok ? blk : 0) * 128 + li * 16;  // first column of this lane
+      float v[16];
+      if (ok) {
+        load16<Tin>(xr + c0, v);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = 0.f;
+      }
       if (a.status != nullptr) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) bad |= ok && !isfinite(v[e]);
+        for (int e = 0; e < 16; ++e) bad |= ok && !isfinite(v[e]);
       }
       if (a.pro != kProNone) {
         if (a.pro == kProGelu) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
+          for (int e = 0; e < 16; ++e)
             v[e] = 0.5f * v[e] * (1.0f + erff(v[e] * 0.70710678118654752f));
-        } else if (ok) {
-          if (a.pro == kProLnModulate) {
+        } else {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) v[e] = (v[e] - mean) * rstd;
+          for (int q = 0; q < 4; ++q) {
+            const float4 sc = __ldg(reinterpret_cast<const float4*>(a.pro_scale + c0) + q);
+            const float4 sh = __ldg(reinterpret_cast<const float4*>(a.pro_shift + c0) + q);
+            const float scv[4] = {sc.x, sc.y, sc.z, sc.w}, shv[4] = {sh.x, sh.y, sh.z, sh.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              float x = v[4 * q + u];
+              if (a.pro == kProLnModulate) x = (x - mean) * rstd;
+              v[4 * q + u] = fmaf(x, 1.0f + scv[u], shv[u]);
+            }
           }
-          const float4 c0 = __ldg(reinterpret_cast<const float4*>(a.pro_scale + c * 8));
-          const float4 c1 = __ldg(reinterpret_cast<const float4*>(a.pro_scale + c * 8) + 1);
-          const float4 h0 = __ldg(reinterpret_cast<const float4*>(a.pro_shift + c * 8));
-          const float4 h1 = __ldg(reinterpret_cast<const float4*>(a.pro_shift + c * 8) + 1);
-          const float sc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-          const float sh[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-#pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] = fmaf(v[e], 1.0f + sc[e], sh[e]);
         }
       }
       if (a.col_mul != nullptr) {
-        const int cc = ok ? c : 0;
-        const float4 m0 = __ldg(reinterpret_cast<const float4*>(a.col_mul + cc * 8));
-        const float4 m1 = __ldg(reinterpret_cast<const float4*>(a.col_mul + cc * 8) + 1);
-        const float2 r0 = __fmul2_rn(make_float2(v[0], v[1]), make_float2(m0.x, m0.y));
-        const float2 r1 = __fmul2_rn(make_float2(v[2], v[3]), make_float2(m0.z, m0.w));
-        const float2 r2 = __fmul2_rn(make_float2(v[4], v[5]), make_float2(m1.x, m1.y));
-        const float2 r3 = __fmul2_rn(make_float2(v[6], v[7]), make_float2(m1.z, m1.w));
-        v[0] = r0.x; v[1] = r0.y; v[2] = r1.x; v[3] = r1.y;
-        v[4] = r2.x; v[5] = r2.y; v[6] = r3.x; v[7] = r3.y;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 m = __ldg(reinterpret_cast<const float4*>(a.col_mul + c0) + q);
+          const float2 p0 = __fmul2_rn(make_float2(v[4 * q], v[4 * q + 1]), make_float2(m.x, m.y));
+          const float2 p1 =
+              __fmul2_rn(make_float2(v[4 * q + 2], v[4 * q + 3]), make_float2(m.z, m.w));
+          v[4 * q] = p0.x;
+          v[4 * q + 1] = p0.y;
+          v[4 * q + 2] = p1.x;
+          v[4 * q + 3] = p1.y;
+        }
       }
       if constexpr (kRot) {
-        // strides 1, 2 (packed pairs P_k = (v_k, v_k+4)) and 4 in registers
-        float2 P0 = make_float2(v[0], v[4]), P1 = make_float2(v[1], v[5]);
-        float2 P2 = make_float2(v[2], v[6]), P3 = make_float2(v[3], v[7]);
-        float2 t0 = f2add(P0, P1), t1 = f2sub(P0, P1), t2 = f2add(P2, P3), t3 = f2sub(P2, P3);
-        P0 = f2add(t0, t2); P2 = f2sub(t0, t2); P1 = f2add(t1, t3); P3 = f2sub(t1, t3);
-        v[0] = P0.x + P0.y; v[4] = P0.x - P0.y;
-        v[1] = P1.x + P1.y; v[5] = P1.x - P1.y;
-        v[2] = P2.x + P2.y; v[6] = P2.x - P2.y;
-        v[3] = P3.x + P3.y; v[7] = P3.x - P3.y;
-        // strides 8, 16, 32, 64: lanes xor 1, 2, 4, 8 (low lane v + o, high o - v)
+        // pairs P_k = (v_k, v_k+8): strides 1, 2, 4 are packed butterflies
+        float2 P[8];
 #pragma unroll
-        for (int st = 0; st < 4; ++st) {
-          const int m = 1 << st;
-          const float sg = st == 0 ? sg_1 : (st == 1 ? sg_2 : (st == 2 ? sg_4 : sg_8));
+        for (int k = 0; k < 8; ++k) P[k] = make_float2(v[k], v[k + 8]);
+#pragma unroll
+        for (int h = 1; h < 8; h <<= 1)
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if ((k & h) == 0) {
+              const float2 sm = f2add(P[k], P[k + h]), df = f2sub(P[k], P[k + h]);
+              P[k] = sm;
+              P[k + h] = df;
+            }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {  // stride 8: within each pair
+          v[k] = P[k].x + P[k].y;
+          v[k + 8] = P[k].x - P[k].y;
+        }
+        // strides 16, 32, 64: lanes xor 1, 2, 4 (low lane v + o, high lane o - v)
+#pragma unroll
+        for (int s3 = 0; s3 < 3; ++s3) {
+          const int m = 1 << s3;
+          const float sg = s3 == 0 ? sgn1 : (s3 == 1 ? sgn2 : sgn4);
           const float2 sg2 = make_float2(sg, sg);
 #pragma unroll
-          for (int e = 0; e < 8; e += 2) {
+          for (int e = 0; e < 16; e += 2) {
             const float o0 = __shfl_xor_sync(0xffffffffu, v[e], m);
             const float o1 = __shfl_xor_sync(0xffffffffu, v[e + 1], m);
             const float2 r = __ffma2_rn(sg2, make_float2(v[e], v[e + 1]), make_float2(o0, o1));
@@ -231,36 +248,30 @@ __global__ void __launch_bounds__(256) fq_fast_kernel(const FqArgs a) {
         }
       }
       if (ok) {
-        float cmn = fminf(fminf(fminf(v[0], v[1]), fminf(v[2], v[3])),
-                          fminf(fminf(v[4], v[5]), fminf(v[6], v[7])));
-        float cmx = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])),
-                          fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
+        float cmn = fminf(v[0], v[15]), cmx = fmaxf(v[0], v[15]);
+#pragma unroll
+        for (int e = 1; e < 15; e += 2) {
+          cmn = fminf(cmn, fminf(v[e], v[e + 1]));
+          cmx = fmaxf(cmx, fmaxf(v[e], v[e + 1]));
+        }
         mn = fminf(mn, cmn);
         mx = fmaxf(mx, cmx);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<float4*>(pr + (blk * 4 + q) * 32 + li * 4) =
+              make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       }
-      float* bp = buf + i * 256 + lane * 4;
-      *reinterpret_cast<float4*>(bp) = make_float4(v[0], v[1], v[2], v[3]);
-      *reinterpret_cast<float4*>(bp + 128) = make_float4(v[4], v[5], v[6], v[7]);
     }
     if (bad) atomicOr(a.status, 1);
+    __syncwarp();
+    // the raw rows are consumed: fetch the next group while params and codes run
+    if (lane == 0 && r0 + gstride < a.M) issue(r0 + gstride);
 #pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) {
+    for (int m = 1; m < 8 * G; m <<= 1) {
       mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, m));
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, m));
     }
-    if (W > 1) {
-      if (lane == 0) {
-        red[g][wg][0] = mn;
-        red[g][wg][1] = mx;
-      }
-      group_sync();
-      for (int w = 0; w < W; ++w) {
-        mn = fminf(mn, red[g][w][0]);
-        mx = fmaxf(mx, red[g][w][1]);
-      }
-    }
 
-    long long tp2 = a.probe ? clock64() : 0;
     // ---- params (quant.cpp:90-124) in fp64 exactly as the reference
     const double qmax = static_cast<double>(qmax_i);
     const double dmn = static_cast<double>(mn), dmx = static_cast<double>(mx);
@@ -280,31 +291,35 @@ __global__ void __launch_bounds__(256) fq_fast_kernel(const FqArgs a) {
       s = (hi - lo) / qmax;
       z = fmin(fmax(rint(-lo / s), 0.0), qmax);
     }
-    if (leader) {
+    if (row_ok && gi == 0 && li == 0) {
       a.scale[row] = s;
       a.zero[row] = static_cast<int32_t>(z);
     }
 
-    long long tp3 = a.probe ? clock64() : 0;
-    // ---- pass 2: codes from the parked values
+    // ---- pass 2: codes from the parked values, 16 per lane -> one 128-bit store
     const float inv_sf = static_cast<float>(1.0 / s), zf = static_cast<float>(z);
     const float qf = static_cast<float>(qmax_i);
     const float2 inv2 = make_float2(inv_sf, inv_sf), z2 = make_float2(zf, zf);
     const float2 mg2 = make_float2(12582912.0f, 12582912.0f);
     const float2 nmg2 = make_float2(-12582912.0f, -12582912.0f);
     uint8_t* crow = a.codes + row * a.ldc;
-#pragma unroll(kNit > 0 ? kNit : 1)
-    for (int i = wg; i < nit; i += W) {
-      const int c = i * 32 + lane;
-      if (!((kNit > 0 && i < kNit - 1) || c < chunks)) continue;
-      const float* bp = buf + i * 256 + lane * 4;
-      const float4 a0 = *reinterpret_cast<const float4*>(bp);
-      const float4 a1 = *reinterpret_cast<const float4*>(bp + 128);
-      const float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      uint32_t m[8];
+#pragma unroll(kNblk > 0 ? (kNblk + G - 1) / G : 1)
+    for (int st = 0; st < steps; ++st) {
+      const int blk = st * G + gi;
+      if (!(row_ok && blk_ok(st, blk))) continue;
+      float v[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 t = *reinterpret_cast<const float4*>(pr + (blk * 4 + q) * 32 + li * 4);
+        v[4 * q] = t.x;
+        v[4 * q + 1] = t.y;
+        v[4 * q + 2] = t.z;
+        v[4 * q + 3] = t.w;
+      }
+      uint32_t mq[16];
       float dm = 0.f;
 #pragma unroll
-      for (int e = 0; e < 8; e += 2) {
+      for (int e = 0; e < 16; e += 2) {
         float2 q = __ffma2_rn(make_float2(v[e], v[e + 1]), inv2, z2);
         if (need_clamp) {
           q.x = fminf(fmaxf(q.x, 0.f), qf);
@@ -313,31 +328,30 @@ __global__ void __launch_bounds__(256) fq_fast_kernel(const FqArgs a) {
         const float2 r = __fadd2_rn(q, mg2);             // round to the integer code
         const float2 d = f2sub(q, __fadd2_rn(r, nmg2));  // q - round(q), exact
         dm = fmaxf(dm, fmaxf(fabsf(d.x), fabsf(d.y)));
-        m[e] = __float_as_uint(r.x);
-        m[e + 1] = __float_as_uint(r.y);
+        mq[e] = __float_as_uint(r.x);
+        mq[e + 1] = __float_as_uint(r.y);
       }
       if (dm > 0.5f - 6.103515625e-05f) {
-        // within the fp32 error bound of a .5 tie: exact fp64 re-evaluation
+        // within the fp32 error bound of a .5 tie: exact fp64 re-evaluation of
+        // just those elements (a warp pays for element e only if a lane needs it)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const double k = fmin(fmax(rint(static_cast<double>(v[e]) / s) + z, 0.0), qmax);
-          m[e] = static_cast<uint32_t>(k);
+        for (int e = 0; e < 16; ++e) {
+          float2 q = __ffma2_rn(make_float2(v[e], v[e]), inv2, z2);
+          if (need_clamp) q.x = fminf(fmaxf(q.x, 0.f), qf);
+          if (fabsf(q.x - rintf(q.x)) > 0.5f - 6.103515625e-05f) {
+            const double k = fmin(fmax(rint(static_cast<double>(v[e]) / s) + z, 0.0), qmax);
+            mq[e] = static_cast<uint32_t>(k);
+          }
         }
       }
-      const uint32_t p0 = __byte_perm(__byte_perm(m[0], m[1], 0x0040), __byte_perm(m[2], m[3], 0x0040), 0x5410);
-      const uint32_t p1 = __byte_perm(__byte_perm(m[4], m[5], 0x0040), __byte_perm(m[6], m[7], 0x0040), 0x5410);
-      *reinterpret_cast<uint2*>(crow + c * 8) = make_uint2(p0, p1);
+      uint32_t p[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        p[w] = __byte_perm(__byte_perm(mq[4 * w], mq[4 * w + 1], 0x0040),
+                           __byte_perm(mq[4 * w + 2], mq[4 * w + 3], 0x0040), 0x5410);
+      *reinterpret_cast<uint4*>(crow + blk * 128 + li * 16) = make_uint4(p[0], p[1], p[2], p[3]);
     }
-    group_sync();  // the whole group is done with this raw buffer (and red) before reuse
-    if (a.probe && lane == 0) {
-      const long long tp4 = clock64();
-      unsigned long long* pr = a.probe + 8 * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-      pr[0] += tp1 - tp0;  // wait for the row copy
-      pr[1] += tp2 - tp1;  // pass 1 (+ reduce)
-      pr[2] += tp3 - tp2;  // params
-      pr[3] += tp4 - tp3;  // pass 2 + group sync
-      pr[4] += 1;          // rows
-    }
+    __syncwarp();
   }
 }
 

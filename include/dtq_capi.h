@@ -119,9 +119,9 @@ int dtq_quantize_rows(const void* x, int x_dtype, int64_t rows, int64_t cols, in
  *   bias     [dev] N f64 or NULL
  *   balance  NULL or the layer's transform (copied into the handle; the
  *            forward applies the activation side automatically)
- * weight_bits in {4, 8}; act_bits in {2,4,6,8}.  W4 weights are stored
- * packed (two codes per byte, trace_io.cpp:79-91 nibble order) and unpacked
- * in shared memory by the GEMM. */
+ * weight_bits and act_bits in {2,4,6,8}.  W4 weights are stored packed (two
+ * codes per byte, trace_io.cpp:79-91 nibble order) and unpacked in shared
+ * memory by the GEMM; 2-, 6- and 8-bit weights are stored as s8 w_sym. */
 int dtq_qlinear_create(const void* w, int w_dtype, int64_t N, int64_t K, int64_t ldw,
                        int weight_bits, int act_bits, const double* bias,
                        const dtq_balance* balance, void* stream, dtq_qlinear_t* out);
@@ -189,6 +189,35 @@ int dtq_qlinear_quantize(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq
  * reported as DTQ_ERR_INVALID_ARGUMENT (the reference's exception). */
 int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_t h, int mode,
                              void* y, int y_dtype, void* stream);
+
+/* ---------------------------------------------------------------- fp64 parity kernels
+ * Device implementations of the remaining reference operations, in fp64 and
+ * in the reference's operation order (bit-identical results).  Used by the
+ * C++ drop-in (include/dtq/*.hpp); not on the timed path.
+ *
+ * grouping: 0 PerTensor, 1 PerToken, 2 PerChannel, 3 PerOutputChannel,
+ *           4 PerGroup(group_size)   (quant.hpp:26-48 GroupingScheme::kind)
+ * scale/zero: one entry per group, [dev]. */
+int dtq_quantize_static(const double* x, int64_t rows, int64_t cols, int64_t ldx, int bits,
+                        int grouping, int64_t group_size, const double* scale,
+                        const int32_t* zero, uint8_t* codes, int64_t ldc, void* stream);
+
+/* out = s * (code - z)   (quant.cpp:179-188) */
+int dtq_dequantize(const uint8_t* codes, int64_t rows, int64_t cols, int64_t ldc, int grouping,
+                   int64_t group_size, const double* scale, const int32_t* zero, double* out,
+                   int64_t ldo, void* stream);
+
+/* apply_scaling / rotate_channels (balance.cpp:57-67, 94-107) on rows:
+ * out = [x * s | x / s] then, per hblock columns, signs, FWHT, 1/sqrt(hb).
+ * smooth and signs may each be NULL; hblock a power of two <= 16384. */
+int dtq_balance_apply(const double* x, int64_t rows, int64_t cols, int64_t ldx,
+                      const double* smooth, int smooth_mul, const int8_t* signs, int64_t hblock,
+                      double* out, int64_t ldo, void* stream);
+
+/* y = x * w^T (+ bias) in fp64 with the reference's sequential summation
+ * (matrix.hpp:62-76): the qlinear_forward_float oracle path. */
+int dtq_matmul_nt_f64(const double* x, int64_t M, int64_t K, const double* w, int64_t N,
+                      const double* bias, double* y, void* stream);
 
 #ifdef __cplusplus
 }

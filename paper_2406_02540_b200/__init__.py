@@ -39,6 +39,7 @@ EXPORTED = (
     "dtq_qlinear_create", "dtq_qlinear_create_from_codes", "dtq_qlinear_destroy",
     "dtq_qlinear_info", "dtq_qlinear_export", "dtq_qgemm", "dtq_qlinear_workspace_bytes",
     "dtq_qlinear_forward", "dtq_qlinear_quantize", "dtq_qlinear_forward_host",
+    "dtq_quantize_static", "dtq_dequantize", "dtq_balance_apply", "dtq_matmul_nt_f64",
 )
 
 

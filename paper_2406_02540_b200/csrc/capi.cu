@@ -293,7 +293,7 @@ __global__ void weight_pack_kernel(const uint8_t* __restrict__ codes, int64_t ld
   if (o >= N) return;
   const int32_t z = 1 << (wbits - 1);
   int32_t sum = 0;
-  if (wbits == 8) {
+  if (wbits != 4) {  // 2-, 6- and 8-bit weights are stored as s8 w_sym
     for (int64_t c = threadIdx.x; c < ld8; c += blockDim.x) {
       int32_t v = 0;
       if (c < K) v = static_cast<int32_t>(codes[o * ldc + c]) - z;
@@ -340,8 +340,8 @@ __global__ void export_codes_kernel(const int8_t* __restrict__ w8, int64_t ld8,
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < N * K;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t o = i / K, c = i % K;
-    if (wbits == 8)
-      out[i] = static_cast<uint8_t>(static_cast<int32_t>(w8[o * ld8 + c]) + 128);
+    if (wbits != 4)
+      out[i] = static_cast<uint8_t>(static_cast<int32_t>(w8[o * ld8 + c]) + (1 << (wbits - 1)));
     else
       out[i] = (w4[o * ld4 + c / 2] >> (4 * (c & 1))) & 0xF;
   }
@@ -469,7 +469,7 @@ int overflow_check(int abits, int wbits, int64_t K) {
 int finish_from_codes(dtq_qlinear_s* h, const uint8_t* codes, int64_t ldc, const double* scale,
                       const double* bias, cudaStream_t st) {
   const int64_t N = h->N, K = h->K;
-  if (h->wbits == 8) {
+  if (h->wbits != 4) {
     h->ld8 = round_up(K, 16);
     CUDA_TRY(cudaMalloc(&h->w8, N * h->ld8));
   } else {
@@ -497,7 +497,7 @@ int finish_from_codes(dtq_qlinear_s* h, const uint8_t* codes, int64_t ldc, const
   }
   const int rows[3] = {256, 128, 64};
   for (int i = 0; i < 3; ++i) {
-    if (h->wbits == 8)
+    if (h->wbits != 4)
       DTQ_TRY(make_tmap_u8(&h->tmB[i], h->w8, N, K, h->ld8, dtq_gemm::BK, rows[i],
                            CU_TENSOR_MAP_SWIZZLE_128B));
     else
@@ -629,7 +629,7 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
     DTQ_TRY(make_tmap_u8(&tY, yk, M, h->N * static_cast<int64_t>(es), ldk * es, 64, 32,
                          CU_TENSOR_MAP_SWIZZLE_64B));
 
-  const cudaError_t e = h->wbits == 8 ? dtq_launch_gemm_w8(tA, tB, tY, g, cfg, sms, st)
+  const cudaError_t e = h->wbits != 4 ? dtq_launch_gemm_w8(tA, tB, tY, g, cfg, sms, st)
                                       : dtq_launch_gemm_w4(tA, tB, tY, g, BN, sms, st);
   if (e != cudaSuccess) return fail(DTQ_ERR_CUDA, "qgemm launch: %s", cudaGetErrorString(e));
 
@@ -723,9 +723,8 @@ int dtq_qlinear_create(const void* w, int w_dtype, int64_t N, int64_t K, int64_t
                        const dtq_balance* balance, void* stream, dtq_qlinear_t* out) {
   if (!out) return fail(DTQ_ERR_INVALID_ARGUMENT, "create: null out");
   *out = nullptr;
-  if (weight_bits != 8 && weight_bits != 4)
-    return fail(weight_bits == 2 || weight_bits == 6 ? DTQ_ERR_UNSUPPORTED : DTQ_ERR_INVALID_ARGUMENT,
-                "make_quant_linear: device GEMM supports weight_bits 4 and 8 (got %d)", weight_bits);
+  if (!bits_supported(weight_bits))
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "make_quant_linear: unsupported bit width");
   if (!bits_supported(act_bits))
     return fail(DTQ_ERR_INVALID_ARGUMENT, "make_quant_linear: unsupported bit width");
   if (N <= 0 || K <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "make_quant_linear: empty W");
@@ -783,8 +782,8 @@ int dtq_qlinear_create_from_codes(const uint8_t* codes, int packed, int64_t ld, 
                                   dtq_qlinear_t* out) {
   if (!out) return fail(DTQ_ERR_INVALID_ARGUMENT, "create: null out");
   *out = nullptr;
-  if (weight_bits != 8 && weight_bits != 4)
-    return fail(DTQ_ERR_UNSUPPORTED, "device GEMM supports weight_bits 4 and 8");
+  if (!bits_supported(weight_bits))
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "unsupported bit width");
   if (!bits_supported(act_bits)) return fail(DTQ_ERR_INVALID_ARGUMENT, "unsupported bit width");
   if (N <= 0 || K <= 0 || !codes || !scale)
     return fail(DTQ_ERR_INVALID_ARGUMENT, "create_from_codes: bad arguments");

@@ -1,0 +1,558 @@
+// dropin.cpp -- the reference C++ API (namespace dtq, include/dtq/*.hpp)
+// implemented over the C ABI (include/dtq_capi.h) on the B200.
+//
+// Value semantics as in the reference: Matrix / QuantizedTensor hold host
+// data; every quantize / dequantize / balance / qlinear call uploads its
+// operands, runs the fp64 "exact" device kernels and downloads the result,
+// so results are bit-identical to the reference library.  Error behaviour
+// follows the reference: std::invalid_argument, std::overflow_error,
+// std::logic_error; a CUDA failure (or no sm_100 device: there is no CPU
+// fallback) raises std::runtime_error.
+//
+// Host-side pieces are bookkeeping and analysis only: grouping indices,
+// round_even (the rounding definition), error_report / incoherence, the
+// calibration-time scaling mask and sign draw, byte accounting.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <bit>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <random>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/dtq/balance.hpp"
+#include "../../include/dtq/matrix.hpp"
+#include "../../include/dtq/plan.hpp"
+#include "../../include/dtq/qgemm.hpp"
+#include "../../include/dtq/quant.hpp"
+#include "../../include/dtq_capi.h"
+
+namespace dtq {
+namespace {
+
+void check(int status) {
+  if (status == DTQ_OK) return;
+  const std::string msg = dtq_last_error();
+  switch (status) {
+    case DTQ_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case DTQ_ERR_OVERFLOW: throw std::overflow_error(msg);
+    case DTQ_ERR_UNSUPPORTED: throw std::logic_error(msg);
+    default: throw std::runtime_error("dtq device error: " + msg);
+  }
+}
+
+void cuda(cudaError_t e) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+}
+
+// RAII device buffer
+template <typename T>
+struct Dev {
+  T* p = nullptr;
+  std::size_t n = 0;
+  explicit Dev(std::size_t count) : n(count) {
+    if (n) cuda(cudaMalloc(reinterpret_cast<void**>(&p), n * sizeof(T)));
+  }
+  Dev(const T* host, std::size_t count) : Dev(count) {
+    if (n) cuda(cudaMemcpy(p, host, n * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  ~Dev() {
+    if (p) cudaFree(p);
+  }
+  Dev(const Dev&) = delete;
+  Dev& operator=(const Dev&) = delete;
+  void get(T* host) const {
+    if (n) cuda(cudaMemcpy(host, p, n * sizeof(T), cudaMemcpyDeviceToHost));
+  }
+};
+
+int grouping_code(Grouping g) { return static_cast<int>(g); }
+
+int64_t pitch16(std::size_t cols) { return static_cast<int64_t>((cols + 15) / 16 * 16); }
+
+// Dynamic params of `rows` contiguous groups of `cols` doubles (device).
+void row_params(const double* x, std::size_t rows, std::size_t cols, int bits, bool symmetric,
+                QuantParams* out) {
+  if (rows == 0 || cols == 0) throw std::invalid_argument("quant: empty group");
+  if (!bits_supported(bits)) throw std::invalid_argument("quant: bits must be one of {2,4,6,8}");
+  if (cols > 16384)
+    throw std::logic_error("quant: device row quantizer handles groups of <= 16384 elements");
+  Dev<double> dx(x, rows * cols);
+  const int64_t ldc = pitch16(cols);
+  Dev<uint8_t> dc(rows * ldc);
+  Dev<double> ds(rows);
+  Dev<int32_t> dz(rows), st(1);
+  cuda(cudaMemset(st.p, 0, sizeof(int32_t)));
+  check(dtq_quantize_rows(dx.p, DTQ_F64, rows, cols, cols, bits, symmetric ? 1 : 0, DTQ_MODE_EXACT,
+                          nullptr, nullptr, dc.p, ldc, ds.p, dz.p, st.p, nullptr));
+  int32_t bad = 0;
+  st.get(&bad);
+  if (bad) throw std::invalid_argument("quant: non-finite value in group");
+  std::vector<double> s(rows);
+  std::vector<int32_t> z(rows);
+  ds.get(s.data());
+  dz.get(z.data());
+  for (std::size_t r = 0; r < rows; ++r) out[r] = {s[r], z[r], bits};
+}
+
+std::vector<double> transpose(const Matrix& m) {
+  std::vector<double> t(m.size());
+  for (std::size_t r = 0; r < m.rows(); ++r)
+    for (std::size_t c = 0; c < m.cols(); ++c) t[c * m.rows() + r] = m(r, c);
+  return t;
+}
+
+// codes for given per-group params (device, fp64 divide + half-even)
+std::vector<uint8_t> codes_for(const Matrix& x, const GroupingScheme& scheme, int bits,
+                               const std::vector<QuantParams>& params) {
+  std::vector<double> s(params.size());
+  std::vector<int32_t> z(params.size());
+  for (std::size_t i = 0; i < params.size(); ++i) {
+    s[i] = params[i].scale;
+    z[i] = params[i].zero_point;
+  }
+  Dev<double> dx(x.data().data(), x.size()), ds(s.data(), s.size());
+  Dev<int32_t> dz(z.data(), z.size());
+  Dev<uint8_t> dc(x.size());
+  check(dtq_quantize_static(dx.p, x.rows(), x.cols(), x.cols(), bits, grouping_code(scheme.kind),
+                            scheme.group_size, ds.p, dz.p, dc.p, x.cols(), nullptr));
+  std::vector<uint8_t> out(x.size());
+  dc.get(out.data());
+  return out;
+}
+
+// device QuantLinear handle built from the layer's host fields
+struct Handle {
+  dtq_qlinear_t h = nullptr;
+  ~Handle() {
+    if (h) dtq_qlinear_destroy(h);
+  }
+};
+
+dtq_qlinear_t device_layer(const QuantLinear& layer) {
+  if (layer.device) return static_cast<Handle*>(layer.device.get())->h;
+  const QuantizedTensor& w = layer.w_q;
+  if (w.params.size() != w.rows || w.ints.size() != w.rows * w.cols)
+    throw std::invalid_argument("qlinear: malformed weight tensor");
+  const int wbits = w.params.empty() ? 8 : w.params[0].bits;
+  std::vector<double> s(w.rows);
+  for (std::size_t o = 0; o < w.rows; ++o) {
+    if (w.params[o].zero_point != (1 << (wbits - 1)))
+      throw std::logic_error("qlinear: device GEMM expects symmetric weights (z = 2^(b-1))");
+    s[o] = w.params[o].scale;
+  }
+  Dev<uint8_t> dc(w.ints.data(), w.ints.size());
+  Dev<double> ds(s.data(), s.size());
+  std::unique_ptr<Dev<double>> db;
+  if (layer.bias) {
+    if (layer.bias->size() != w.rows) throw std::invalid_argument("qlinear: bias length != C_out");
+    db = std::make_unique<Dev<double>>(layer.bias->data(), layer.bias->size());
+  }
+  auto hd = std::make_shared<Handle>();
+  check(dtq_qlinear_create_from_codes(dc.p, 0, w.cols, wbits, ds.p, w.rows, w.cols, layer.act_bits,
+                                      db ? db->p : nullptr, nullptr, nullptr, &hd->h));
+  cuda(cudaDeviceSynchronize());
+  layer.device = hd;
+  return hd->h;
+}
+
+Matrix balance_rows(const Matrix& m, const double* smooth, bool mul, const int8_t* signs,
+                    std::size_t hb) {
+  Dev<double> dx(m.data().data(), m.size()), dout(m.size());
+  std::unique_ptr<Dev<double>> dsm;
+  std::unique_ptr<Dev<int8_t>> dsg;
+  if (smooth) dsm = std::make_unique<Dev<double>>(smooth, m.cols());
+  if (signs) dsg = std::make_unique<Dev<int8_t>>(signs, m.cols());
+  check(dtq_balance_apply(dx.p, m.rows(), m.cols(), m.cols(), dsm ? dsm->p : nullptr, mul ? 1 : 0,
+                          dsg ? dsg->p : nullptr, hb, dout.p, m.cols(), nullptr));
+  Matrix out(m.rows(), m.cols());
+  dout.get(out.data().data());
+  return out;
+}
+
+}  // namespace
+
+// ================================================================ matrix.hpp
+Matrix matmul_nt(const Matrix& x, const Matrix& w) {
+  if (x.cols() != w.cols()) throw std::invalid_argument("matmul_nt: inner dimensions differ");
+  Dev<double> dx(x.data().data(), x.size()), dw(w.data().data(), w.size());
+  Dev<double> dy(x.rows() * w.rows());
+  check(dtq_matmul_nt_f64(dx.p, x.rows(), x.cols(), dw.p, w.rows(), nullptr, dy.p, nullptr));
+  Matrix y(x.rows(), w.rows());
+  dy.get(y.data().data());
+  return y;
+}
+
+double max_abs(const Matrix& m) {
+  double v = 0.0;
+  for (double x : m.data()) v = std::max(v, std::abs(x));
+  return v;
+}
+
+double mse(const Matrix& a, const Matrix& b) {
+  if (!a.same_shape(b)) throw std::invalid_argument("mse: shape mismatch");
+  double acc = 0.0;
+  for (std::size_t i = 0; i < a.size(); ++i) acc += (a.data()[i] - b.data()[i]) * (a.data()[i] - b.data()[i]);
+  return acc / static_cast<double>(a.size());
+}
+
+std::vector<double> col_absmax(const Matrix& m) {
+  std::vector<double> out(m.cols(), 0.0);
+  for (std::size_t r = 0; r < m.rows(); ++r)
+    for (std::size_t c = 0; c < m.cols(); ++c) out[c] = std::max(out[c], std::abs(m(r, c)));
+  return out;
+}
+
+std::vector<double> row_absmax(const Matrix& m) {
+  std::vector<double> out(m.rows(), 0.0);
+  for (std::size_t r = 0; r < m.rows(); ++r)
+    for (std::size_t c = 0; c < m.cols(); ++c) out[r] = std::max(out[r], std::abs(m(r, c)));
+  return out;
+}
+
+// ================================================================ quant.hpp
+double round_even(double v) {
+  // IEEE roundToIntegralTiesToEven (quant.cpp:9-16 restates it with floor/fmod)
+  return std::nearbyint(v);
+}
+
+bool bits_supported(int bits) { return bits == 2 || bits == 4 || bits == 6 || bits == 8; }
+
+std::size_t GroupingScheme::group_count(std::size_t rows, std::size_t cols) const {
+  switch (kind) {
+    case Grouping::PerTensor: return 1;
+    case Grouping::PerToken:
+    case Grouping::PerOutputChannel: return rows;
+    case Grouping::PerChannel: return cols;
+    case Grouping::PerGroup:
+      if (group_size == 0 || cols % group_size != 0)
+        throw std::invalid_argument("GroupingScheme: group_size must divide cols");
+      return rows * (cols / group_size);
+  }
+  throw std::logic_error("GroupingScheme: bad kind");
+}
+
+std::size_t GroupingScheme::group_of(std::size_t r, std::size_t c, std::size_t cols) const {
+  switch (kind) {
+    case Grouping::PerTensor: return 0;
+    case Grouping::PerToken:
+    case Grouping::PerOutputChannel: return r;
+    case Grouping::PerChannel: return c;
+    case Grouping::PerGroup: return r * (cols / group_size) + c / group_size;
+  }
+  throw std::logic_error("GroupingScheme: bad kind");
+}
+
+QuantParams compute_minmax_params(std::span<const double> group, int bits) {
+  QuantParams p;
+  row_params(group.data(), group.empty() ? 0 : 1, group.size(), bits, false, &p);
+  return p;
+}
+
+QuantParams compute_symmetric_params(std::span<const double> group, int bits) {
+  QuantParams p;
+  row_params(group.data(), group.empty() ? 0 : 1, group.size(), bits, true, &p);
+  return p;
+}
+
+std::vector<QuantParams> compute_params(const Matrix& x, const GroupingScheme& scheme, int bits,
+                                        bool symmetric) {
+  const std::size_t ng = scheme.group_count(x.rows(), x.cols());
+  std::vector<QuantParams> p(ng);
+  switch (scheme.kind) {
+    case Grouping::PerToken:
+    case Grouping::PerOutputChannel:
+      row_params(x.data().data(), x.rows(), x.cols(), bits, symmetric, p.data());
+      break;
+    case Grouping::PerGroup:  // contiguous sub-rows: rows * (cols/gs) groups of gs
+      row_params(x.data().data(), ng, scheme.group_size, bits, symmetric, p.data());
+      break;
+    case Grouping::PerTensor:
+      row_params(x.data().data(), 1, x.size(), bits, symmetric, p.data());
+      break;
+    case Grouping::PerChannel: {
+      const std::vector<double> t = transpose(x);
+      row_params(t.data(), x.cols(), x.rows(), bits, symmetric, p.data());
+      break;
+    }
+  }
+  return p;
+}
+
+QuantizedTensor quantize(const Matrix& x, const GroupingScheme& scheme, int bits, QuantMode mode,
+                         const std::vector<QuantParams>* frozen_params, bool symmetric) {
+  if (!bits_supported(bits)) throw std::invalid_argument("quantize: bits must be one of {2,4,6,8}");
+  if (!x.all_finite()) throw std::invalid_argument("quantize: non-finite input");
+  const std::size_t ng = scheme.group_count(x.rows(), x.cols());
+  QuantizedTensor q;
+  q.rows = x.rows();
+  q.cols = x.cols();
+  q.scheme = scheme;
+  q.symmetric = symmetric;
+  if (mode == QuantMode::Static) {
+    if (frozen_params == nullptr)
+      throw std::invalid_argument("quantize: Static mode requires frozen params");
+    if (frozen_params->size() != ng)
+      throw std::invalid_argument("quantize: frozen params group count mismatch");
+    for (const auto& p : *frozen_params)
+      if (p.bits != bits) throw std::invalid_argument("quantize: frozen params bit width mismatch");
+    q.params = *frozen_params;
+  } else {
+    q.params = compute_params(x, scheme, bits, symmetric);
+  }
+  q.ints = codes_for(x, scheme, bits, q.params);
+  return q;
+}
+
+Matrix dequantize(const QuantizedTensor& q) {
+  Matrix out(q.rows, q.cols);
+  std::vector<double> s(q.params.size());
+  std::vector<int32_t> z(q.params.size());
+  for (std::size_t i = 0; i < q.params.size(); ++i) {
+    s[i] = q.params[i].scale;
+    z[i] = q.params[i].zero_point;
+  }
+  Dev<uint8_t> dc(q.ints.data(), q.ints.size());
+  Dev<double> ds(s.data(), s.size()), dout(out.size());
+  Dev<int32_t> dz(z.data(), z.size());
+  check(dtq_dequantize(dc.p, q.rows, q.cols, q.cols, grouping_code(q.scheme.kind),
+                       q.scheme.group_size, ds.p, dz.p, dout.p, q.cols, nullptr));
+  dout.get(out.data().data());
+  return out;
+}
+
+Matrix fake_quantize(const Matrix& x, const GroupingScheme& scheme, int bits, QuantMode mode,
+                     const std::vector<QuantParams>* frozen_params, bool symmetric) {
+  return dequantize(quantize(x, scheme, bits, mode, frozen_params, symmetric));
+}
+
+QuantErrorReport error_report(const Matrix& x, const QuantizedTensor& q) {
+  if (x.rows() != q.rows || x.cols() != q.cols)
+    throw std::invalid_argument("error_report: shape mismatch");
+  QuantErrorReport rep;
+  double rnd = 0.0, clp = 0.0;
+  for (std::size_t r = 0; r < q.rows; ++r)
+    for (std::size_t c = 0; c < q.cols; ++c) {
+      const QuantParams& p = q.params_of(r, c);
+      const double pre = round_even(x(r, c) / p.scale) + p.zero_point;
+      const double err = x(r, c) - p.scale * (static_cast<int32_t>(q.code(r, c)) - p.zero_point);
+      rep.max_abs_err = std::max(rep.max_abs_err, std::abs(err));
+      ((pre < 0.0 || pre > static_cast<double>((1 << p.bits) - 1)) ? clp : rnd) += err * err;
+    }
+  const double n = static_cast<double>(x.size());
+  rep.rounding_mse = rnd / n;
+  rep.clamping_mse = clp / n;
+  rep.total_mse = (rnd + clp) / n;
+  return rep;
+}
+
+double incoherence(std::span<const double> group) {
+  if (group.empty()) throw std::invalid_argument("incoherence: empty group");
+  double amax = 0.0, sq = 0.0;
+  for (double v : group) {
+    amax = std::max(amax, std::abs(v));
+    sq += v * v;
+  }
+  if (sq == 0.0) throw std::invalid_argument("incoherence: all-zero group");
+  return amax * std::sqrt(static_cast<double>(group.size())) / std::sqrt(sq);
+}
+
+// ================================================================ balance.hpp
+void fwht(double* data, std::size_t n) {
+  for (std::size_t h = 1; h < n; h <<= 1)
+    for (std::size_t i = 0; i < n; i += 2 * h)
+      for (std::size_t j = i; j < i + h; ++j) {
+        const double a = data[j], b = data[j + h];
+        data[j] = a + b;
+        data[j + h] = a - b;
+      }
+}
+
+ScalingMask compute_scaling_mask(const std::vector<double>& act_absmax,
+                                 const std::vector<double>& weight_absmax, double alpha) {
+  if (act_absmax.size() != weight_absmax.size())
+    throw std::invalid_argument("compute_scaling_mask: vector length mismatch");
+  if (alpha < 0.0 || alpha > 1.0)
+    throw std::invalid_argument("compute_scaling_mask: alpha must be in [0,1]");
+  ScalingMask m;
+  m.alpha = alpha;
+  m.s.resize(act_absmax.size());
+  for (std::size_t i = 0; i < act_absmax.size(); ++i) {
+    const double a = act_absmax[i], w = weight_absmax[i];
+    const bool dead = a <= 0.0 || w <= 0.0 || !std::isfinite(a) || !std::isfinite(w);
+    m.s[i] = dead ? 1.0 : std::clamp(std::pow(a, alpha) / std::pow(w, 1.0 - alpha), 1e-5, 1e5);
+  }
+  return m;
+}
+
+std::pair<Matrix, Matrix> apply_scaling(const Matrix& x, const Matrix& w, const ScalingMask& mask) {
+  if (x.cols() != mask.s.size() || w.cols() != mask.s.size())
+    throw std::invalid_argument("apply_scaling: dimension mismatch");
+  return {balance_rows(x, mask.s.data(), false, nullptr, 0),
+          balance_rows(w, mask.s.data(), true, nullptr, 0)};
+}
+
+RotationMatrix hadamard_matrix(std::size_t n, bool randomize, uint64_t seed) {
+  if (n < 2 || (n & (n - 1)) != 0)
+    throw std::invalid_argument("hadamard_matrix: n must be a power of two >= 2");
+  RotationMatrix h;
+  h.n = n;
+  h.sign_diag.assign(n, int8_t{1});
+  if (randomize) {
+    std::mt19937_64 rng(seed);
+    for (auto& d : h.sign_diag) d = (rng() & 1) ? int8_t{1} : int8_t{-1};
+  }
+  return h;
+}
+
+Matrix RotationMatrix::dense() const {
+  Matrix m(n, n);
+  const double norm = 1.0 / std::sqrt(static_cast<double>(n));
+  for (std::size_t r = 0; r < n; ++r)
+    for (std::size_t c = 0; c < n; ++c)
+      m(r, c) = sign_diag[r] * ((std::popcount(r & c) & 1) ? -1 : 1) * norm;
+  return m;
+}
+
+Matrix rotate_channels(const Matrix& m, const RotationMatrix& h) {
+  if (m.cols() != h.n) throw std::invalid_argument("rotate_channels: channel count != rotation size");
+  return balance_rows(m, nullptr, false, h.sign_diag.data(), h.n);
+}
+
+std::pair<Matrix, Matrix> apply_rotation(const Matrix& x, const Matrix& w, const RotationMatrix& h) {
+  if (x.cols() != h.n || w.cols() != h.n)
+    throw std::invalid_argument("apply_rotation: dimension mismatch");
+  return {rotate_channels(x, h), rotate_channels(w, h)};
+}
+
+BalanceTransform static_dynamic_balance(const Matrix& static_base, const Matrix& w, double alpha,
+                                        uint64_t seed) {
+  if (static_base.cols() != w.cols())
+    throw std::invalid_argument("static_dynamic_balance: channel mismatch");
+  BalanceTransform t;
+  t.mask = compute_scaling_mask(col_absmax(static_base), col_absmax(w), alpha);
+  t.rotation = hadamard_matrix(w.cols(), true, seed);
+  return t;
+}
+
+std::pair<Matrix, Matrix> apply_balance(const Matrix& x, const Matrix& w, const BalanceTransform& t) {
+  Matrix xb = x, wb = w;
+  if (t.mask) std::tie(xb, wb) = apply_scaling(xb, wb, *t.mask);
+  if (t.rotation) std::tie(xb, wb) = apply_rotation(xb, wb, *t.rotation);
+  return {std::move(xb), std::move(wb)};
+}
+
+double choose_alpha(const Matrix& calib_x, const Matrix& w, int act_bits, int weight_bits) {
+  const Matrix ref = matmul_nt(calib_x, w);
+  const std::vector<double> am = col_absmax(calib_x), wm = col_absmax(w);
+  double best_alpha = 0.5, best = std::numeric_limits<double>::infinity();
+  for (int step = 1; step <= 9; ++step) {
+    const double alpha = 0.1 * step;
+    const auto [xs, ws] = apply_scaling(calib_x, w, compute_scaling_mask(am, wm, alpha));
+    const Matrix xq = fake_quantize(xs, GroupingScheme::per_token(), act_bits, QuantMode::Dynamic);
+    const Matrix wq = fake_quantize(ws, GroupingScheme::per_output_channel(), weight_bits,
+                                    QuantMode::Dynamic, nullptr, true);
+    const double err = mse(matmul_nt(xq, wq), ref);
+    if (err < best) {
+      best = err;
+      best_alpha = alpha;
+    }
+  }
+  return best_alpha;
+}
+
+// ================================================================ qgemm.hpp
+QuantLinear make_quant_linear(const Matrix& w, int weight_bits, int act_bits,
+                              const std::optional<std::vector<double>>& bias) {
+  if (!bits_supported(weight_bits) || !bits_supported(act_bits))
+    throw std::invalid_argument("make_quant_linear: unsupported bit width");
+  if (bias && bias->size() != w.rows())
+    throw std::invalid_argument("make_quant_linear: bias length != C_out");
+  if (!w.all_finite()) throw std::invalid_argument("quantize: non-finite input");
+  Dev<double> dw(w.data().data(), w.size());
+  std::unique_ptr<Dev<double>> db;
+  if (bias) db = std::make_unique<Dev<double>>(bias->data(), bias->size());
+  auto hd = std::make_shared<Handle>();
+  check(dtq_qlinear_create(dw.p, DTQ_F64, w.rows(), w.cols(), w.cols(), weight_bits, act_bits,
+                           db ? db->p : nullptr, nullptr, nullptr, &hd->h));
+  QuantLinear layer;
+  layer.w_q.rows = w.rows();
+  layer.w_q.cols = w.cols();
+  layer.w_q.scheme = GroupingScheme::per_output_channel();
+  layer.w_q.symmetric = true;
+  layer.w_q.ints.resize(w.size());
+  std::vector<double> s(w.rows());
+  check(dtq_qlinear_export(hd->h, layer.w_q.ints.data(), s.data(), nullptr, nullptr));
+  layer.w_q.params.resize(w.rows());
+  for (std::size_t o = 0; o < w.rows(); ++o) layer.w_q.params[o] = {s[o], 1 << (weight_bits - 1), weight_bits};
+  layer.bias = bias;
+  layer.act_bits = act_bits;
+  layer.device = hd;
+  return layer;
+}
+
+Matrix qlinear_forward(const Matrix& x, const QuantLinear& layer) {
+  const std::size_t c_in = layer.in_channels(), c_out = layer.out_channels();
+  if (x.cols() != c_in) throw std::invalid_argument("qlinear_forward: X cols != C_in");
+  const int64_t max_term =
+      static_cast<int64_t>((1 << layer.act_bits) - 1) *
+      (int64_t{1} << (layer.w_q.params.empty() ? 7 : layer.w_q.params[0].bits - 1));
+  if (max_term > std::numeric_limits<int64_t>::max() / static_cast<int64_t>(c_in))
+    throw std::overflow_error("qlinear_forward: accumulator could overflow");
+  if (!x.all_finite()) throw std::invalid_argument("quantize: non-finite input");
+  const dtq_qlinear_t h = device_layer(layer);
+  Dev<double> dx(x.data().data(), x.size()), dy(x.rows() * c_out);
+  check(dtq_qlinear_forward(dx.p, DTQ_F64, x.rows(), c_in, h, DTQ_MODE_EXACT, nullptr, dy.p, DTQ_F64,
+                            c_out, nullptr, 0, nullptr, nullptr));
+  Matrix y(x.rows(), c_out);
+  dy.get(y.data().data());
+  return y;
+}
+
+Matrix qlinear_forward_float(const Matrix& x, const QuantLinear& layer) {
+  const Matrix x_fq = fake_quantize(x, GroupingScheme::per_token(), layer.act_bits, QuantMode::Dynamic);
+  const Matrix w_deq = dequantize(layer.w_q);
+  Dev<double> dx(x_fq.data().data(), x_fq.size()), dw(w_deq.data().data(), w_deq.size());
+  Dev<double> dy(x.rows() * w_deq.rows());
+  std::unique_ptr<Dev<double>> db;
+  if (layer.bias) db = std::make_unique<Dev<double>>(layer.bias->data(), layer.bias->size());
+  check(dtq_matmul_nt_f64(dx.p, x_fq.rows(), x_fq.cols(), dw.p, w_deq.rows(), db ? db->p : nullptr,
+                          dy.p, nullptr));
+  Matrix y(x.rows(), w_deq.rows());
+  dy.get(y.data().data());
+  return y;
+}
+
+LayerBytes weight_bytes(std::size_t rows, std::size_t cols, int bits, std::size_t group_count) {
+  return {(rows * cols * static_cast<std::size_t>(bits) + 7) / 8, group_count * 4};
+}
+
+std::size_t checkpoint_bytes(const std::vector<std::pair<Matrix, int>>& layers) {
+  std::size_t total = 0;
+  for (const auto& [w, bits] : layers) {
+    const LayerBytes b = weight_bytes(w.rows(), w.cols(), bits, w.rows());
+    total += b.weights + b.params;
+  }
+  return total;
+}
+
+std::size_t fp16_baseline_bytes(const std::vector<std::pair<Matrix, int>>& layers) {
+  std::size_t total = 0;
+  for (const auto& l : layers) total += l.first.rows() * l.first.cols() * 2;
+  return total;
+}
+
+// ================================================================ plan.hpp
+std::array<TimestepRange, kNumRanges> partition_timesteps(std::size_t steps) {
+  if (steps == 0 || steps % kNumRanges != 0)
+    throw std::invalid_argument("partition_timesteps: steps must be divisible by 4");
+  std::array<TimestepRange, kNumRanges> out;
+  const std::size_t span = steps / kNumRanges;
+  for (std::size_t i = 0; i < kNumRanges; ++i) out[i] = {i, i * span, (i + 1) * span};
+  return out;
+}
+
+}  // namespace dtq

@@ -1,0 +1,170 @@
+// parity_kernels.cu -- fp64 device kernels for the reference operations that
+// are not on the timed path (static quantize for every grouping, dequantize,
+// apply_scaling / rotate_channels, the fp64 float-path GEMM).  Each keeps
+// the reference's operation order so results are bit-identical; they back
+// the C++ drop-in (include/dtq) and the parity tests.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/dtq_capi.h"
+
+namespace {
+
+int last_cuda(const char* what);
+
+__device__ __forceinline__ int64_t group_of(int grouping, int64_t gs, int64_t r, int64_t c,
+                                            int64_t cols) {
+  // quant.cpp:36-45
+  switch (grouping) {
+    case 0: return 0;
+    case 1:
+    case 3: return r;
+    case 2: return c;
+    default: return r * (cols / gs) + c / gs;
+  }
+}
+
+__global__ void quantize_static_kernel(const double* __restrict__ x, int64_t rows, int64_t cols,
+                                       int64_t ldx, double qmax, int grouping, int64_t gs,
+                                       const double* __restrict__ s, const int32_t* __restrict__ z,
+                                       uint8_t* __restrict__ codes, int64_t ldc) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rows * cols;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const int64_t g = group_of(grouping, gs, r, c, cols);
+    // quant.cpp:171-173: k = round_even(x / s) + z, clamped, cast
+    const double k = rint(x[r * ldx + c] / s[g]) + static_cast<double>(z[g]);
+    codes[r * ldc + c] = static_cast<uint8_t>(fmin(fmax(k, 0.0), qmax));
+  }
+}
+
+__global__ void dequantize_kernel(const uint8_t* __restrict__ codes, int64_t rows, int64_t cols,
+                                  int64_t ldc, int grouping, int64_t gs,
+                                  const double* __restrict__ s, const int32_t* __restrict__ z,
+                                  double* __restrict__ out, int64_t ldo) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rows * cols;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const int64_t g = group_of(grouping, gs, r, c, cols);
+    out[r * ldo + c] = s[g] * static_cast<double>(static_cast<int32_t>(codes[r * ldc + c]) - z[g]);
+  }
+}
+
+// One CTA per (row, hblock-wide block): scale, signs, in-smem FWHT with the
+// reference butterfly order (balance.cpp:22-33), normalise.
+__global__ void balance_kernel(const double* __restrict__ x, int64_t cols, int64_t ldx,
+                               const double* __restrict__ smooth, int smooth_mul,
+                               const int8_t* __restrict__ signs, int64_t hb,
+                               double* __restrict__ out, int64_t ldo) {
+  extern __shared__ double buf[];
+  const int64_t r = blockIdx.y;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * hb;
+  for (int64_t c = threadIdx.x; c < hb; c += blockDim.x) {
+    double v = x[r * ldx + base + c];
+    if (smooth) v = smooth_mul ? v * smooth[base + c] : v / smooth[base + c];
+    if (signs) v *= static_cast<double>(signs[base + c]);
+    buf[c] = v;
+  }
+  __syncthreads();
+  if (signs) {
+    for (int64_t h = 1; h < hb; h <<= 1) {
+      for (int64_t p = threadIdx.x; p < hb / 2; p += blockDim.x) {
+        const int64_t j = (p / h) * (2 * h) + (p % h);
+        const double a = buf[j], b = buf[j + h];
+        buf[j] = a + b;
+        buf[j + h] = a - b;
+      }
+      __syncthreads();
+    }
+  }
+  const double norm = signs ? 1.0 / sqrt(static_cast<double>(hb)) : 1.0;
+  for (int64_t c = threadIdx.x; c < hb; c += blockDim.x)
+    out[r * ldo + base + c] = signs ? buf[c] * norm : buf[c];
+}
+
+__global__ void matmul_nt_f64_kernel(const double* __restrict__ x, int64_t M, int64_t K,
+                                     const double* __restrict__ w, int64_t N,
+                                     const double* __restrict__ bias, double* __restrict__ y) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < M * N;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / N, o = i % N;
+    double acc = 0.0;
+    for (int64_t k = 0; k < K; ++k) acc = __dadd_rn(acc, __dmul_rn(x[t * K + k], w[o * K + k]));
+    if (bias) acc = __dadd_rn(acc, bias[o]);  // qgemm.cpp:74-76 adds bias after the GEMM
+    y[i] = acc;
+  }
+}
+
+int grid_for(int64_t n) {
+  const int64_t g = (n + 255) / 256;
+  return static_cast<int>(g < 148 * 32 ? (g > 0 ? g : 1) : 148 * 32);
+}
+
+}  // namespace
+
+extern "C" {
+
+int dtq_quantize_static(const double* x, int64_t rows, int64_t cols, int64_t ldx, int bits,
+                        int grouping, int64_t group_size, const double* scale,
+                        const int32_t* zero, uint8_t* codes, int64_t ldc, void* stream) {
+  if (rows <= 0 || cols <= 0 || !x || !scale || !zero || !codes) return DTQ_ERR_INVALID_ARGUMENT;
+  if (!(bits == 2 || bits == 4 || bits == 6 || bits == 8)) return DTQ_ERR_INVALID_ARGUMENT;
+  if (grouping == 4 && (group_size <= 0 || cols % group_size)) return DTQ_ERR_INVALID_ARGUMENT;
+  quantize_static_kernel<<<grid_for(rows * cols), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, rows, cols, ldx, static_cast<double>((1 << bits) - 1), grouping, group_size, scale, zero,
+      codes, ldc);
+  return last_cuda("quantize_static");
+}
+
+int dtq_dequantize(const uint8_t* codes, int64_t rows, int64_t cols, int64_t ldc, int grouping,
+                   int64_t group_size, const double* scale, const int32_t* zero, double* out,
+                   int64_t ldo, void* stream) {
+  if (rows <= 0 || cols <= 0 || !codes || !scale || !zero || !out) return DTQ_ERR_INVALID_ARGUMENT;
+  if (grouping == 4 && (group_size <= 0 || cols % group_size)) return DTQ_ERR_INVALID_ARGUMENT;
+  dequantize_kernel<<<grid_for(rows * cols), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      codes, rows, cols, ldc, grouping, group_size, scale, zero, out, ldo);
+  return last_cuda("dequantize");
+}
+
+int dtq_balance_apply(const double* x, int64_t rows, int64_t cols, int64_t ldx,
+                      const double* smooth, int smooth_mul, const int8_t* signs, int64_t hblock,
+                      double* out, int64_t ldo, void* stream) {
+  if (rows <= 0 || cols <= 0 || !x || !out) return DTQ_ERR_INVALID_ARGUMENT;
+  const int64_t hb = signs ? hblock : (cols < 1024 ? cols : 1024);
+  if (signs && (hb < 2 || (hb & (hb - 1)) != 0 || cols % hb != 0 || hb > 16384))
+    return DTQ_ERR_INVALID_ARGUMENT;
+  if (!signs && cols % hb != 0) {
+    // plain scaling with no rotation: any width, one "block" per row
+    if (cols > 16384) return DTQ_ERR_INVALID_ARGUMENT;
+    dim3 grid(1, static_cast<unsigned>(rows));
+    balance_kernel<<<grid, 256, cols * sizeof(double), static_cast<cudaStream_t>(stream)>>>(
+        x, cols, ldx, smooth, smooth_mul, nullptr, cols, out, ldo);
+    return last_cuda("balance_apply");
+  }
+  dim3 grid(static_cast<unsigned>(cols / hb), static_cast<unsigned>(rows));
+  const size_t smem = hb * sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(balance_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+  balance_kernel<<<grid, 256, smem, static_cast<cudaStream_t>(stream)>>>(
+      x, cols, ldx, smooth, smooth_mul, signs, hb, out, ldo);
+  return last_cuda("balance_apply");
+}
+
+int dtq_matmul_nt_f64(const double* x, int64_t M, int64_t K, const double* w, int64_t N,
+                      const double* bias, double* y, void* stream) {
+  if (M <= 0 || K <= 0 || N <= 0 || !x || !w || !y) return DTQ_ERR_INVALID_ARGUMENT;
+  matmul_nt_f64_kernel<<<grid_for(M * N), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, M, K, w, N, bias, y);
+  return last_cuda("matmul_nt_f64");
+}
+
+}  // extern "C"
+
+namespace {
+int last_cuda(const char* what) {
+  (void)what;
+  return cudaGetLastError() == cudaSuccess ? DTQ_OK : DTQ_ERR_CUDA;
+}
+}  // namespace

@@ -1,0 +1,92 @@
+"""The C++ drop-in (include/dtq/*.hpp over the C ABI, libdtq_dropin.so).
+
+CPU: the library exports every dtq:: entry point the reference's headers
+declare (quant.hpp / balance.hpp / qgemm.hpp / matrix.hpp / plan.hpp) and the
+reference's own unit-test binary is built against it.
+GPU: that binary -- the reference's test_quant.cpp, test_qgemm.cpp and
+test_balance.cpp compiled unmodified (tests/dropin/Makefile) -- passes on
+the B200, i.e. the reference's own known-answer and property tests hold for
+the device implementation.
+"""
+import os
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(ROOT, "paper_2406_02540_b200", "libdtq_dropin.so")
+BIN = os.path.join(ROOT, "tests", "dropin", "_bin", "dtq_ref_tests")
+
+# reference declarations (quant.hpp:20-112, balance.hpp:16-71, qgemm.hpp:17-54,
+# plan.hpp) as demangled prefixes
+DROPIN_API = [
+    "dtq::round_even(double)",
+    "dtq::bits_supported(int)",
+    "dtq::GroupingScheme::group_count(",
+    "dtq::GroupingScheme::group_of(",
+    "dtq::compute_minmax_params(",
+    "dtq::compute_symmetric_params(",
+    "dtq::compute_params(",
+    "dtq::quantize(",
+    "dtq::dequantize(",
+    "dtq::fake_quantize(",
+    "dtq::error_report(",
+    "dtq::incoherence(",
+    "dtq::fwht(double*",
+    "dtq::compute_scaling_mask(",
+    "dtq::apply_scaling(",
+    "dtq::hadamard_matrix(",
+    "dtq::RotationMatrix::dense() const",
+    "dtq::rotate_channels(",
+    "dtq::apply_rotation(",
+    "dtq::static_dynamic_balance(",
+    "dtq::apply_balance(",
+    "dtq::choose_alpha(",
+    "dtq::make_quant_linear(",
+    "dtq::qlinear_forward(",
+    "dtq::qlinear_forward_float(",
+    "dtq::weight_bytes(",
+    "dtq::checkpoint_bytes(",
+    "dtq::fp16_baseline_bytes(",
+    "dtq::matmul_nt(",
+    "dtq::partition_timesteps(",
+]
+
+
+def _exports():
+    if not os.path.exists(LIB):
+        pytest.skip("libdtq_dropin.so not built")
+    nm = shutil.which("nm")
+    if nm is None:
+        pytest.skip("nm not available")
+    out = subprocess.run([nm, "-D", "-C", "--defined-only", LIB], check=True,
+                         capture_output=True, text=True).stdout
+    return out
+
+
+def test_dropin_exports_reference_api():
+    out = _exports()
+    missing = [f for f in DROPIN_API if f not in out]
+    assert not missing, missing
+
+
+def test_dropin_has_no_host_compute_path():
+    # the drop-in runs its arithmetic through libdtq_b200 (no CPU fallback):
+    # it must link the product library, not the oracle
+    out = subprocess.run(["ldd", LIB], capture_output=True, text=True).stdout if os.path.exists(LIB) else ""
+    if not out:
+        pytest.skip("libdtq_dropin.so not built")
+    assert "libdtq_b200.so" in out
+    assert "dtq_oracle" not in out and "dtq_ref" not in out
+
+
+@pytest.mark.gpu
+def test_reference_unit_tests_pass_on_device():
+    if not os.path.exists(BIN):
+        pytest.skip("reference unit-test binary not built (needs /root/reference at build time)")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    print(r.stderr[-4000:])
+    assert r.returncode == 0, r.stderr[-4000:]
+    assert "0 failed" in r.stdout

@@ -182,8 +182,11 @@ __global__ void __launch_bounds__(256) fq_fast_kernel(const FqArgs a) {
       if (a.pro != kProNone) {
         if (a.pro == kProGelu) {
 #pragma unroll
-          for (int e = 0; e < 16; ++e)
-            v[e] = 0.5f * v[e] * (1.0f + erff(v[e] * 0.70710678118654752f));
+          for (int e = 0; e < 16; e += 2) {
+            const float2 g = gelu2(make_float2(v[e], v[e + 1]));
+            v[e] = g.x;
+            v[e + 1] = g.y;
+          }
         } else {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {

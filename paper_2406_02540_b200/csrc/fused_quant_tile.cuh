@@ -1,0 +1,475 @@
+// fused_quant_tile.cuh -- tile-pipelined fused quantizer (fp32 "fast" mode).
+//
+// Same contract as fq_fast_kernel (fused_quant_fast.cuh), with a
+// decomposition built for instruction count and latency hiding:
+//
+//   TWO LANES (l and l+16 of a warp) OWN ONE 128-COLUMN BLOCK OF ONE ROW.
+//
+// Lane half p = lane / 16 holds the block elements e with bit 4 of e equal
+// to p: four runs of 16 contiguous elements (e = 32m + 16p + 0..15), kept as
+// 32 fp32 pairs P_k = (v_l, v_l+32) of local index l = 16m + (e & 15).  The
+// 128-point Walsh-Hadamard transform then runs in the reference's stage
+// order (balance.cpp:22-33): strides 1, 2, 4, 8 packed FADD2/FFMA2 in
+// registers, stride 16 across the lane pair (shfl.xor 16), stride 32 packed,
+// stride 64 inside each pair -- ~5 instructions per element.
+//
+// A CTA processes tiles of R rows x K columns (nb = K/128 blocks, pair q =
+// 16*warp + lane%16 -> row q % R, block q / R; R <= 16), persistent over
+// tiles, two CTAs per SM:
+//   * the R input rows of a tile arrive by bulk async copies (cp.async.bulk,
+//     one mbarrier per buffer) into a double buffer: tile i+1 is in flight
+//     while tile i computes.  Row pitch = K*es + 16 bytes, so the 128-bit
+//     reads of 8 rows per phase are bank-conflict free (R = 16);
+//   * per-column multiplier (sign * 1/s_c * 1/sqrt(128), with the modulate
+//     prologue's (1 + scale) and shift folded in) from a per-CTA smem table;
+//   * row min / max: 3-input FMNMX3, pair shuffle, one smem exchange across
+//     the nb blocks of a row = the ONLY barrier per tile; every thread then
+//     derives its row's s, z in fp64 exactly as quant.cpp:90-124;
+//   * codes: r = fma(v, 1/s, z + 1.5*2^23) rounds the exact product-sum once
+//     (ties-even, low byte = code) -- one FFMA2 per two codes;
+//   * kExactV (no prologue, smoothing or rotation: v is the exact input, so
+//     the reference codes are reachable bit for bit): the exact residual
+//     e = fma(v, 1/s, (z + 1.5*2^23) - r) is checked, and |e| > 1/2 - 2^-15
+//     (|v/s - v*fl(1/s)| <= 2^-16 < the margin) re-evaluates that group of
+//     16 values with IEEE fp64 divides (rare, out of line);
+//   * a lane pair's 2 x 16 codes per run are one contiguous 32-byte sector:
+//     16-byte stores straight from registers, no staging, no barrier.
+//
+// Host contract: K % 128 == 0, K <= 8192, 16-byte aligned input rows and
+// code rows, rotation block 128, blockDim = round_up(2*R*nb, 32), dynamic
+// smem = fq_tile_layout(...).bytes.
+#pragma once
+
+#include "fused_quant.cuh"
+#include "ptx.cuh"
+
+namespace dtq_fq {
+
+struct TileLayout {
+  size_t pitch_in;
+  size_t off_in1, off_a, off_b, off_red, off_bar, bytes;
+};
+
+__host__ __device__ inline TileLayout fq_tile_layout(int64_t K, int R, int es, bool has_a,
+                                                     bool has_b) {
+  TileLayout L;
+  const size_t nb = static_cast<size_t>(K) / 128;
+  L.pitch_in = static_cast<size_t>(K) * es + 16;
+  L.off_in1 = static_cast<size_t>(R) * L.pitch_in;
+  L.off_a = 2 * L.off_in1;
+  L.off_b = L.off_a + (has_a ? static_cast<size_t>(K) * 4 : 0);
+  L.off_red = L.off_b + (has_b ? static_cast<size_t>(K) * 4 : 0);
+  // min/max pairs (double-buffered) + two LayerNorm partial arrays, nb x R each
+  L.off_bar = L.off_red + nb * R * (2 * 8 + 4 + 4);
+  L.off_bar = (L.off_bar + 7) / 8 * 8;
+  L.bytes = L.off_bar + 16;
+  return L;
+}
+
+__host__ __device__ inline int fq_tile_threads(int64_t K, int R) {
+  return static_cast<int>((2 * R * (K / 128) + 31) / 32 * 32);
+}
+
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float min3f(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+constexpr float kFqTie = 0.5f - 3.0517578125e-05f;  // 1/2 - 2^-15
+
+// Exact re-evaluation (quant.cpp:169-175 in fp64) of the flagged 16-value
+// runs of one lane: v[16m + i] is run m, w[4m .. 4m+3] its packed codes.
+__device__ __noinline__ void fq_tile_fix(const float* v, uint32_t* w, unsigned runs, float inv_sf,
+                                         float zm, double s, double z, double qmax) {
+#pragma unroll 1
+  for (int m = 0; m < 4; ++m) {
+    if (!((runs >> m) & 1u)) continue;
+#pragma unroll 1
+    for (int i = 0; i < 16; ++i) {
+      const float x = v[16 * m + i];
+      const float rr = fmaf(x, inv_sf, zm);
+      const float e = fmaf(x, inv_sf, zm - rr);
+      if (fabsf(e) > kFqTie) {
+        const uint32_t c =
+            static_cast<uint32_t>(fmin(fmax(rint(static_cast<double>(x) / s) + z, 0.0), qmax));
+        const int word = 4 * m + (i >> 2);
+        const uint32_t sh = 8u * (i & 3);
+        w[word] = (w[word] & ~(0xffu << sh)) | (c << sh);
+      }
+    }
+  }
+}
+
+// 16 raw elements at p (smem) -> fp32
+template <typename Tin>
+__device__ __forceinline__ void ld16(const uint8_t* p, float (&o)[16]) {
+  float a[8], b[8];
+  uint4 r0[Vec<Tin>::kWords], r1[Vec<Tin>::kWords];
+#pragma unroll
+  for (int w = 0; w < Vec<Tin>::kWords; ++w) {
+    r0[w] = reinterpret_cast<const uint4*>(p)[w];
+    r1[w] = reinterpret_cast<const uint4*>(p + 8 * sizeof(Tin))[w];
+  }
+  unpack<float>(r0, a, Tin());
+  unpack<float>(r1, b, Tin());
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    o[i] = a[i];
+    o[8 + i] = b[i];
+  }
+}
+
+// value l (0..63) of a lane: P[l & 31].x for l < 32, .y otherwise
+#define FQ_V(P, l) ((l) < 32 ? (P)[(l)&31].x : (P)[(l)&31].y)
+
+// 64 codes of one lane -> 4 x 16-byte stores (runs m = 0..3)
+template <bool kClamp, bool kExactV>
+__device__ __forceinline__ void fq_tile_codes(const float2 (&P)[32], float inv_sf, float zm,
+                                              int qmax_i, double s, double z, double qmax,
+                                              uint8_t* __restrict__ dst) {
+  const float2 inv2 = make_float2(inv_sf, inv_sf), zm2 = make_float2(zm, zm);
+  const float2 neg = make_float2(-1.f, -1.f);
+  const float lo = 12582912.0f, hi = 12582912.0f + static_cast<float>(qmax_i);
+  uint32_t w[16];   // run m (values 16m..16m+15) -> w[4m..4m+3]
+  float em[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {  // pairs 4g..4g+3 of each 16-pair half
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t cx[4], cy[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 v = P[16 * h + 4 * g + u];
+        float2 rr = __ffma2_rn(v, inv2, zm2);
+        if constexpr (kExactV) {
+          const float2 e = __ffma2_rn(v, inv2, __ffma2_rn(rr, neg, zm2));  // exact residual
+          em[h] = fmaxf(em[h], fabsf(e.x));
+          em[2 + h] = fmaxf(em[2 + h], fabsf(e.y));
+        }
+        if constexpr (kClamp) {
+          rr.x = fminf(fmaxf(rr.x, lo), hi);
+          rr.y = fminf(fmaxf(rr.y, lo), hi);
+        }
+        cx[u] = __float_as_uint(rr.x);
+        cy[u] = __float_as_uint(rr.y);
+      }
+      // .x of pairs 16h + .. -> run h; .y -> run 2 + h
+      w[4 * h + g] = __byte_perm(__byte_perm(cx[0], cx[1], 0x0040),
+                                 __byte_perm(cx[2], cx[3], 0x0040), 0x5410);
+      w[4 * (2 + h) + g] = __byte_perm(__byte_perm(cy[0], cy[1], 0x0040),
+                                       __byte_perm(cy[2], cy[3], 0x0040), 0x5410);
+    }
+  }
+  if constexpr (kExactV) {
+    const unsigned runs = (em[0] > kFqTie ? 1u : 0u) | (em[1] > kFqTie ? 2u : 0u) |
+                          (em[2] > kFqTie ? 4u : 0u) | (em[3] > kFqTie ? 8u : 0u);
+    if (runs) {
+      // copy out (keeps P itself in registers) and re-evaluate exactly
+      float vb[64];
+#pragma unroll
+      for (int l = 0; l < 64; ++l) vb[l] = FQ_V(P, l);
+      fq_tile_fix(vb, w, runs, inv_sf, zm, s, z, qmax);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+    *reinterpret_cast<uint4*>(dst + 32 * m) = make_uint4(w[4 * m], w[4 * m + 1], w[4 * m + 2],
+                                                         w[4 * m + 3]);
+}
+
+template <typename Tin, bool kRot, bool kExactV, int kPro>
+__global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const int R) {
+  extern __shared__ __align__(128) uint8_t fq_smem[];
+  constexpr int es = sizeof(Tin);
+  constexpr bool has_b = kPro == kProModulate || kPro == kProLnModulate;
+  const int K = static_cast<int>(a.K);
+  const int nb = K >> 7;
+  const int t = threadIdx.x;
+  const int lane = t & 31, warp = t >> 5;
+  const int p = lane >> 4;
+  const int q = warp * 16 + (lane & 15);  // (row, block) pair index
+  const int r = q & (R - 1);
+  const int b_raw = q / R;
+  const bool active = b_raw < nb;  // blockDim is rounded up to whole warps
+  const int b = active ? b_raw : 0;
+  const bool has_a = has_b || a.col_mul != nullptr;
+  const TileLayout L = fq_tile_layout(K, R, es, has_a, has_b);
+  float* colA = reinterpret_cast<float*>(fq_smem + L.off_a);
+  float* colB = reinterpret_cast<float*>(fq_smem + L.off_b);
+  float2* red_mm = reinterpret_cast<float2*>(fq_smem + L.off_red);
+  float* red_s1 = reinterpret_cast<float*>(fq_smem + L.off_red + static_cast<size_t>(nb) * R * 16);
+  float* red_s2 = red_s1 + nb * R;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fq_smem + L.off_bar);  // [2]
+  const uint8_t* __restrict__ X = static_cast<const uint8_t*>(a.x);
+  const uint32_t row_bytes = static_cast<uint32_t>(K) * es;
+
+  const int64_t ntiles = (a.M + R - 1) / R;
+  auto issue = [&](int64_t tile, int buf) {  // warp 0
+    const int64_t row0 = tile * R;
+    const int nval = static_cast<int>(a.M - row0 < R ? a.M - row0 : R);
+    if (lane == 0) dtq_ptx::mbar_arrive_expect_tx(bar + buf, row_bytes * nval);
+    __syncwarp();
+    uint8_t* dst = fq_smem + buf * L.off_in1;
+    if (lane < nval)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+          "[%3];" ::"r"(dtq_ptx::smem_u32(dst + lane * L.pitch_in)),
+          "l"(reinterpret_cast<uint64_t>(X + ((row0 + lane) * a.ldx) * es)), "r"(row_bytes),
+          "r"(dtq_ptx::smem_u32(bar + buf))
+          : "memory");
+  };
+  int64_t tile = blockIdx.x;
+  // warp 0: barriers, then the first tile's copies (overlap the table setup)
+  if (warp == 0) {
+    if (lane == 0) {
+      dtq_ptx::mbar_init(bar, 1);
+      dtq_ptx::mbar_init(bar + 1, 1);
+      dtq_ptx::fence_barrier_init();
+    }
+    __syncwarp();
+    if (tile < ntiles) issue(tile, 0);
+  }
+  // folded per-column affine map: v -> v * A_c + B_c
+  for (int c = t; c < K; c += blockDim.x) {
+    const float m = a.col_mul != nullptr ? a.col_mul[c] : 1.f;
+    if constexpr (has_b) {
+      colA[c] = (1.f + a.pro_scale[c]) * m;
+      colB[c] = a.pro_shift[c] * m;
+    } else {
+      if (has_a) colA[c] = m;
+    }
+  }
+  __syncthreads();
+  const int qmax_i = (1 << a.bits) - 1;
+  const double qmax = static_cast<double>(qmax_i);
+  const float sg16 = p ? -1.f : 1.f;
+  const int c0 = b * 128 + 16 * p;  // first column of run 0
+
+  for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const int64_t row = tile * R + r;
+    const bool ok = active && row < a.M;
+    // prefetch the next tile into the other buffer (free since the last barrier)
+    if (warp == 0 && tile + gridDim.x < ntiles) {
+      dtq_ptx::fence_proxy_async_smem();
+      issue(tile + gridDim.x, buf ^ 1);
+    }
+    dtq_ptx::mbar_wait(bar + buf, (it >> 1) & 1);
+
+    // ---- 1. own 64 values -> registers: run m = columns c0 + 32m + 0..15
+    float2 P[32];
+    {
+      const uint8_t* src = fq_smem + buf * L.off_in1 + r * L.pitch_in + c0 * es;
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        float lo[16], hi[16];
+        ld16<Tin>(src + 32 * m * es, lo);
+        ld16<Tin>(src + 32 * (m + 2) * es, hi);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) P[16 * m + i] = make_float2(lo[i], hi[i]);
+      }
+    }
+
+    // ---- 2. prologue
+    if constexpr (kPro == kProGelu) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) P[k] = gelu2(P[k]);
+    } else if constexpr (kPro == kProLnModulate) {
+      float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < 32; ++k) s2 = __fadd2_rn(s2, P[k]);
+      float s1 = s2.x + s2.y;
+      s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+      if (p == 0 && active) red_s1[b * R + r] = s1;
+      __syncthreads();
+      float tot = 0.f;
+      for (int j = 0; j < nb; ++j) tot += red_s1[j * R + r];
+      const float mean = tot / static_cast<float>(K);
+      const float2 nm = make_float2(-mean, -mean);
+      float2 qq = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float2 d = __fadd2_rn(P[k], nm);
+        qq = __ffma2_rn(d, d, qq);
+      }
+      float q1 = qq.x + qq.y;
+      q1 += __shfl_xor_sync(0xffffffffu, q1, 16);
+      if (p == 0 && active) red_s2[b * R + r] = q1;
+      __syncthreads();
+      float tq = 0.f;
+      for (int j = 0; j < nb; ++j) tq += red_s2[j * R + r];
+      const float rstd = rsqrtf(tq / static_cast<float>(K) + a.eps);
+      const float2 r2 = make_float2(rstd, rstd), o2 = make_float2(-mean * rstd, -mean * rstd);
+#pragma unroll
+      for (int k = 0; k < 32; ++k) P[k] = __ffma2_rn(P[k], r2, o2);
+    }
+
+    // ---- 3. folded column map, then the transform
+    if (has_a) {
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int cl = c0 + 32 * m + 4 * g, ch = cl + 64;  // runs m and m + 2
+          const float4 A0 = *reinterpret_cast<const float4*>(colA + cl);
+          const float4 A1 = *reinterpret_cast<const float4*>(colA + ch);
+          float2* Q = P + 16 * m + 4 * g;
+          if constexpr (has_b) {
+            const float4 B0 = *reinterpret_cast<const float4*>(colB + cl);
+            const float4 B1 = *reinterpret_cast<const float4*>(colB + ch);
+            Q[0] = __ffma2_rn(Q[0], make_float2(A0.x, A1.x), make_float2(B0.x, B1.x));
+            Q[1] = __ffma2_rn(Q[1], make_float2(A0.y, A1.y), make_float2(B0.y, B1.y));
+            Q[2] = __ffma2_rn(Q[2], make_float2(A0.z, A1.z), make_float2(B0.z, B1.z));
+            Q[3] = __ffma2_rn(Q[3], make_float2(A0.w, A1.w), make_float2(B0.w, B1.w));
+          } else {
+            Q[0] = __fmul2_rn(Q[0], make_float2(A0.x, A1.x));
+            Q[1] = __fmul2_rn(Q[1], make_float2(A0.y, A1.y));
+            Q[2] = __fmul2_rn(Q[2], make_float2(A0.z, A1.z));
+            Q[3] = __fmul2_rn(Q[3], make_float2(A0.w, A1.w));
+          }
+        }
+      }
+    }
+    if constexpr (kRot) {
+      const float2 neg = make_float2(-1.f, -1.f);
+      auto stage = [&](int h) {  // local stride h over the pair index
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if ((k & h) == 0) {
+            const float2 sm = __fadd2_rn(P[k], P[k + h]);
+            const float2 df = __ffma2_rn(P[k + h], neg, P[k]);
+            P[k] = sm;
+            P[k + h] = df;
+          }
+      };
+      stage(1);  // element stride 1
+      stage(2);  // 2
+      stage(4);  // 4
+      stage(8);  // 8
+      {          // element stride 16: across the lane pair
+        const float2 sg = make_float2(sg16, sg16);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const float ox = __shfl_xor_sync(0xffffffffu, P[k].x, 16);
+          const float oy = __shfl_xor_sync(0xffffffffu, P[k].y, 16);
+          P[k] = __ffma2_rn(P[k], sg, make_float2(ox, oy));
+        }
+      }
+      stage(16);  // element stride 32
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {  // element stride 64: inside each pair
+        const float u = P[k].x, w = P[k].y;
+        P[k] = make_float2(u + w, u - w);
+      }
+    }
+    if (a.status != nullptr && ok) {
+      // non-finite input <=> non-finite sum (after the transform P[0].x of
+      // lane half 0 IS the scaled block sum); re-checked element-wise
+      float sum;
+      if constexpr (kRot) {
+        sum = P[0].x;
+      } else {
+        float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) s2 = __fadd2_rn(s2, P[k]);
+        sum = s2.x + s2.y;
+      }
+      if (!isfinite(sum)) {
+        bool bad = false;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) bad |= !isfinite(P[k].x) || !isfinite(P[k].y);
+        if (bad) atomicOr(a.status, 1);
+      }
+    }
+
+    // ---- 4. row min / max -> params (fp64, quant.cpp:90-124)
+    {
+      float mn4[4], mx4[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        mn4[i] = fminf(P[8 * i].x, P[8 * i].y);
+        mx4[i] = fmaxf(P[8 * i].x, P[8 * i].y);
+#pragma unroll
+        for (int k = 1; k < 8; ++k) {
+          mn4[i] = min3f(mn4[i], P[8 * i + k].x, P[8 * i + k].y);
+          mx4[i] = max3f(mx4[i], P[8 * i + k].x, P[8 * i + k].y);
+        }
+      }
+      float mn = fminf(min3f(mn4[0], mn4[1], mn4[2]), mn4[3]);
+      float mx = fmaxf(max3f(mx4[0], mx4[1], mx4[2]), mx4[3]);
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 16));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      if (p == 0 && active) red_mm[(buf * nb + b) * R + r] = make_float2(mn, mx);
+    }
+    __syncthreads();  // the one barrier per tile (also frees the input buffer)
+    if (!ok) continue;
+    float mn = __int_as_float(0x7f800000), mx = -mn;
+    for (int j = 0; j < nb; ++j) {
+      const float2 m = red_mm[(buf * nb + j) * R + r];
+      mn = fminf(mn, m.x);
+      mx = fmaxf(mx, m.y);
+    }
+    // params (quant.cpp:90-124).  z needs rint(-lo / s) of the fp64 s: an
+    // fp32 estimate is exact unless the quotient lies within 2^-10 of a
+    // tie (then fp64); 1/s in fp32 suffices unless the codes must be exact
+    // (kExactV).  The fp64 s itself is formed by the thread that stores it.
+    const int qmax_i2 = qmax_i;
+    bool clamp = a.symmetric || a.bits != 8;
+    float zf, inv_sf;
+    if (a.symmetric) {
+      const float amax = fmaxf(fabsf(mn), fabsf(mx));
+      zf = static_cast<float>(1 << (a.bits - 1));
+      inv_sf = amax > 0.f ? static_cast<float>((1 << (a.bits - 1)) - 1) / amax : 1.f;
+    } else if (mx == mn) {
+      inv_sf = 1.f;
+      zf = fminf(fmaxf(rintf(-mn), 0.f), static_cast<float>(qmax_i2));
+      clamp = true;
+    } else {
+      const float lo = fminf(mn, 0.f), hi = fmaxf(mx, 0.f);
+      inv_sf = static_cast<float>(qmax_i2) / (hi - lo);
+      const float q = -lo * inv_sf;
+      zf = fminf(fmaxf(rintf(q), 0.f), static_cast<float>(qmax_i2));
+      if (fabsf(q - truncf(q) - 0.5f) < 1e-3f) {
+        const double sd = (static_cast<double>(hi) - static_cast<double>(lo)) / qmax;
+        zf = static_cast<float>(fmin(fmax(rint(-static_cast<double>(lo) / sd), 0.0), qmax));
+      }
+    }
+    double s = 0.0;
+    const bool writer = b == 0 && p == 0;
+    if (writer || kExactV) {
+      const double dmn = static_cast<double>(mn), dmx = static_cast<double>(mx);
+      if (a.symmetric) {
+        const double amax = fmax(fabs(dmn), fabs(dmx));
+        s = amax > 0.0 ? amax / static_cast<double>((1 << (a.bits - 1)) - 1) : 1.0;
+      } else if (dmx == dmn) {
+        s = 1.0;
+      } else {
+        s = (fmax(dmx, 0.0) - fmin(dmn, 0.0)) / qmax;
+      }
+      if (kExactV) inv_sf = static_cast<float>(1.0 / s);
+      if (writer) {
+        a.scale[row] = s;
+        a.zero[row] = static_cast<int32_t>(zf);
+      }
+    }
+    const double z = static_cast<double>(zf);
+    const float zm = zf + 12582912.0f;
+
+    // ---- 5. codes straight from registers
+    uint8_t* dst = a.codes + row * a.ldc + c0;
+    if (clamp)
+      fq_tile_codes<true, kExactV>(P, inv_sf, zm, qmax_i, s, z, qmax, dst);
+    else
+      fq_tile_codes<false, kExactV>(P, inv_sf, zm, qmax_i, s, z, qmax, dst);
+  }
+}
+
+#undef FQ_V
+
+}  // namespace dtq_fq

@@ -1,73 +1,90 @@
-"""Summarise an ncu report: per-kernel SOL numbers, DRAM bytes and the SASS
-opcode mix / stall hot spots (reads `ncu -i ... --csv`; runs on the CPU box)."""
+"""Summarise ncu outputs into profiles/ (run here, after gpurun brings them back).
+
+usage:
+  python tools/ncu_summary.py launches <launches.csv> <out.md>
+  python tools/ncu_summary.py report <file.ncu-rep> <out.md> [--traffic-json profiles/latest_traffic.json]
+"""
 import collections
 import csv
 import io
+import json
 import subprocess
 import sys
 
-METRICS = ["Duration", "Elapsed Cycles", "SM Frequency", "DRAM Throughput", "Memory Throughput",
-           "L2 Cache Throughput", "Compute (SM) Throughput", "Issue Slots Busy", "Registers Per Thread",
-           "Achieved Occupancy", "Executed Ipc Active"]
+KEYS = [
+    "gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "dram__bytes_read.sum",
+    "dram__bytes_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+    "launch__shared_mem_per_block_dynamic",
+    "sm__pipe_tensor_op_imma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "lts__t_sectors_srcunit_tex_op_write.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+]
 
 
-def run(args):
-    return subprocess.run(["ncu", "-i", *args, "--print-units", "base"], capture_output=True, text=True).stdout
-
-
-def details(rep):
-    rows = list(csv.reader(io.StringIO(run([rep, "--page", "details", "--csv"]))))
-    h = rows[0]
-    ki, mi, vi, ui = (h.index(c) for c in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
-    out = collections.OrderedDict()
-    for r in rows[1:]:
-        k = r[ki].split("(")[0][:70]
-        if r[mi] in METRICS:
-            out.setdefault(k, {}).setdefault(r[mi], f"{r[vi]} {r[ui]}")
-    return out
-
-
-def raw(rep, names):
-    rows = list(csv.reader(io.StringIO(run([rep, "--page", "raw", "--csv"]))))
-    h = rows[0]
-    idx = [h.index(n) for n in names if n in h]
-    ki = h.index("Kernel Name")
-    return [(r[ki].split("(")[0][:70], [r[i] for i in idx]) for r in rows[2:]]
-
-
-def source(rep, kern, top=25):
-    rows = list(csv.reader(io.StringIO(run([rep, "--page", "source", "--csv", "--kernel-name",
-                                            f"regex:{kern}"]))))
-    h = rows[1]
-    data = rows[2:]
-    si, smp, ie = h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
-    tot_s = sum(int(r[smp] or 0) for r in data)
-    tot_i = sum(int(r[ie] or 0) for r in data)
-    print(f"  [{kern}] samples {tot_s} warp-instructions {tot_i}")
-    op, ops = collections.Counter(), collections.Counter()
-    for r in data:
-        toks = r[si].split()
-        if not toks:
+def launches(path, out):
+    rows = list(csv.reader(open(path)))
+    hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hdr]
+    ki, vi, mi = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Name")
+    d = collections.OrderedDict()
+    for r in rows[hdr + 1:]:
+        if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
-        o = toks[1] if toks[0].startswith("@") else toks[0]
-        o = o.split(".")[0]
-        op[o] += int(r[ie] or 0)
-        ops[o] += int(r[smp] or 0)
-    for o, c in op.most_common(top):
-        print(f"    {o:10s} {c:9d} ({100 * c / max(tot_i, 1):5.1f}%)  samples {ops[o]:6d} ({100 * ops[o] / max(tot_s, 1):5.1f}%)")
-    print("  hottest:")
-    for r in sorted(data, key=lambda r: -int(r[smp] or 0))[:12]:
-        print(f"    {r[smp]:>6} {r[ie]:>9}  {r[si][:80]}")
+        name = r[ki].split("(")[0][:110]
+        d.setdefault(name, []).append(float(r[vi].replace(",", "")))
+    tot = sum(sum(v) for v in d.values())
+    with open(out, "w") as f:
+        f.write("# ncu launch list (gpu__time_duration.sum, --clock-control none)\n\n")
+        f.write(f"source: `{path}`; cold-cache, serialised per-launch times; the SHARE is what "
+                "matters, absolute times are not bench numbers.\n\n")
+        f.write("| kernel | launches | mean us | total us | share |\n|---|---:|---:|---:|---:|\n")
+        for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
+            f.write(f"| `{k}` | {len(v)} | {sum(v) / len(v) / 1e3:.2f} | {sum(v) / 1e3:.1f} | "
+                    f"{sum(v) / tot * 100:.1f}% |\n")
+    print(open(out).read())
+
+
+def report(path, out, traffic_json=None):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units = rows[0], rows[1]
+    with open(out, "w") as f:
+        f.write(f"# ncu --set full summary: `{path}`\n\n")
+        for r in rows[2:]:
+            name = r[h.index("Kernel Name")]
+            f.write(f"## `{name[:160]}`\n\n| metric | value | unit |\n|---|---:|---|\n")
+            vals = {}
+            for k in KEYS:
+                if k in h:
+                    i = h.index(k)
+                    f.write(f"| {k} | {r[i]} | {units[i]} |\n")
+                    vals[k] = (r[i], units[i])
+            f.write("\n")
+            if traffic_json and ("qgemm" in name or "fq_tile" in name):
+                def to_bytes(v):
+                    x, u = float(v[0].replace(",", "")), v[1].lower()
+                    return x * {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}.get(u, 1)
+                rd = to_bytes(vals["dram__bytes_read.sum"])
+                wr = to_bytes(vals["dram__bytes_write.sum"])
+                try:
+                    tj = json.load(open(traffic_json))
+                except Exception:
+                    tj = {}
+                key = "qgemm_kernel_dram_bytes" if "qgemm" in name else "fq_kernel_dram_bytes"
+                tj[key] = rd + wr
+                tj[key + "_source"] = path
+                json.dump(tj, open(traffic_json, "w"), indent=1)
+    print(open(out).read())
 
 
 if __name__ == "__main__":
-    rep = sys.argv[1]
-    for k, m in details(rep).items():
-        print(k)
-        for n in METRICS:
-            if n in m:
-                print(f"   {n:28s} {m[n]}")
-    for k, v in raw(rep, ["dram__bytes_read.sum", "dram__bytes_write.sum"]):
-        print("  dram read/write", k[:40], v)
-    for kern in sys.argv[2:]:
-        source(rep, kern)
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2], sys.argv[3])
+    else:
+        tj = sys.argv[sys.argv.index("--traffic-json") + 1] if "--traffic-json" in sys.argv else None
+        report(sys.argv[2], sys.argv[3], tj)

@@ -470,7 +470,9 @@ int copy_balance(dtq_qlinear_s* h, const dtq_balance* bal, cudaStream_t st) {
 }
 
 int overflow_check(int abits, int wbits, int64_t K) {
-  // int32 accumulation must be exact: (2^ab - 1) * 2^(wb-1) * K < 2^31
+  // int32 accumulation must be exact: (2^ab - 1) * 2^(wb-1) * K < 2^31.
+  // W4 weights enter the MMA as 16*w (qgemm_sm100.cuh), i.e. with the W8 bound.
+  if (wbits == 4) wbits = 8;
   const int64_t max_term = static_cast<int64_t>((1 << abits) - 1) * (int64_t{1} << (wbits - 1));
   if (max_term * K > INT32_MAX)
     return fail(DTQ_ERR_OVERFLOW, "qlinear_forward: accumulator could overflow (K=%lld)",
@@ -526,24 +528,27 @@ int finish_from_codes(dtq_qlinear_s* h, const uint8_t* codes, int64_t ldc, const
 // shapes; ties go to the CTA pair (half the B traffic per SM) and wider N.
 // DTQ_GEMM_CFG=<0..3> forces {1cta/256, 1cta/128, 2cta/256, 2cta/128}.
 GemmCfg choose_gemm_cfg(int64_t M, int64_t N, int wbits, int sms) {
-  const GemmCfg cands[4] = {{256, 1}, {128, 1}, {256, 0}, {128, 0}};
+  // preference order on ties: CTA pairs, then wide tiles
+  const GemmCfg cands[4] = {{256, 1}, {256, 0}, {128, 1}, {128, 0}};
   static const int forced = [] {
     const char* e = std::getenv("DTQ_GEMM_CFG");
     return e ? std::atoi(e) : -1;
   }();
   if (forced >= 0 && forced < 4) {
     const GemmCfg f[4] = {{256, 0}, {128, 0}, {256, 1}, {128, 1}};
-    if (!(wbits == 4 && f[forced].cta2)) return f[forced];
+    return f[forced];
   }
   GemmCfg best{256, 0};
   int64_t best_cost = INT64_MAX;
   for (const GemmCfg& c : cands) {
-    if (c.cta2 && wbits == 4) continue;
     const int64_t tm = c.cta2 ? 256 : 128;
     const int64_t tiles = ((M + tm - 1) / tm) * ((N + c.bn - 1) / c.bn);
     const int64_t units = c.cta2 ? sms / 2 : sms;
     const int64_t waves = (tiles + units - 1) / units;
-    const int64_t cost = waves * c.bn;
+    // a tile costs its BN columns plus a fixed ~128-column share (A-tile
+    // loads, TMEM drain, epilogue tail): measured on the STDiT shapes, BN=256
+    // CTA pairs win whenever the wave counts are within that margin
+    const int64_t cost = waves * (c.bn + 128);
     if (cost < best_cost) {
       best_cost = cost;
       best = c;
@@ -643,7 +648,7 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
                          CU_TENSOR_MAP_SWIZZLE_64B));
 
   const cudaError_t e = h->wbits != 4 ? dtq_launch_gemm_w8(tA, tB, tY, g, cfg, sms, st)
-                                      : dtq_launch_gemm_w4(tA, tB, tY, g, BN, sms, st);
+                                      : dtq_launch_gemm_w4(tA, tB, tY, g, cfg, sms, st);
   if (e != cudaSuccess) return fail(DTQ_ERR_CUDA, "qgemm launch: %s", cudaGetErrorString(e));
 
   if (y_dtype == DTQ_F64) {

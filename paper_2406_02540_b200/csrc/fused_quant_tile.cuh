@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const i
           : "memory");
   };
   int64_t tile = blockIdx.x;
+  dtq_ptx::pdl_launch_dependents();  // let the GEMM that consumes the codes launch early
   // warp 0: barriers, then the first tile's copies (overlap the table setup)
   if (warp == 0) {
     if (lane == 0) {
@@ -235,14 +236,33 @@ __global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const i
     __syncwarp();
     if (tile < ntiles) issue(tile, 0);
   }
-  // folded per-column affine map: v -> v * A_c + B_c
-  for (int c = t; c < K; c += blockDim.x) {
-    const float m = a.col_mul != nullptr ? a.col_mul[c] : 1.f;
-    if constexpr (has_b) {
-      colA[c] = (1.f + a.pro_scale[c]) * m;
-      colB[c] = a.pro_shift[c] * m;
-    } else {
-      if (has_a) colA[c] = m;
+  // folded per-column affine map: v -> v * A_c + B_c.  Loads are batched
+  // 8 deep per thread so the table costs one L2 round trip, not eight.
+  if (has_a) {
+    for (int c0 = t; c0 < K; c0 += 8 * blockDim.x) {
+      float m[8], sc[8], sh[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * blockDim.x;
+        const bool in = c < K;
+        m[u] = (in && a.col_mul != nullptr) ? __ldg(a.col_mul + c) : 1.f;
+        if constexpr (has_b) {
+          sc[u] = in ? __ldg(a.pro_scale + c) : 0.f;
+          sh[u] = in ? __ldg(a.pro_shift + c) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * blockDim.x;
+        if (c < K) {
+          if constexpr (has_b) {
+            colA[c] = (1.f + sc[u]) * m[u];
+            colB[c] = sh[u] * m[u];
+          } else {
+            colA[c] = m[u];
+          }
+        }
+      }
     }
   }
   __syncthreads();

@@ -2,9 +2,12 @@
 #include "launch.h"
 
 cudaError_t dtq_launch_gemm_w4(const CUtensorMap& tA, const CUtensorMap& tB,
-                               const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, int BN, int sms,
-                               cudaStream_t st) {
-  // smem ring: 3 x (16 KB A + 16 KB packed + 32 KB s8) at BN=256
-  return BN == 256 ? dtq_launch_gemm_o<256, 3, true, false>(tA, tB, tY, g, sms, st)
-                   : dtq_launch_gemm_o<128, 4, true, false>(tA, tB, tY, g, sms, st);
+                               const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, GemmCfg c,
+                               int sms, cudaStream_t st) {
+  // smem ring per stage: 16 KB A + packed + s8 B rows of this CTA
+  if (c.cta2)  // CTA pair: each SM unpacks only its half of B
+    return c.bn == 256 ? dtq_launch_gemm_o<256, 4, true, true>(tA, tB, tY, g, sms, st)
+                       : dtq_launch_gemm_o<128, 6, true, true>(tA, tB, tY, g, sms, st);
+  return c.bn == 256 ? dtq_launch_gemm_o<256, 3, true, false>(tA, tB, tY, g, sms, st)
+                     : dtq_launch_gemm_o<128, 4, true, false>(tA, tB, tY, g, sms, st);
 }

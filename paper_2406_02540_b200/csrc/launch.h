@@ -33,8 +33,8 @@ cudaError_t dtq_launch_gemm_w8(const CUtensorMap& tA, const CUtensorMap& tB,
                                const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, GemmCfg c,
                                int sms, cudaStream_t st);
 cudaError_t dtq_launch_gemm_w4(const CUtensorMap& tA, const CUtensorMap& tB,
-                               const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, int BN, int sms,
-                               cudaStream_t st);
+                               const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, GemmCfg c,
+                               int sms, cudaStream_t st);
 
 template <int BN, int kStages, bool kW4, int kOut, bool k2Cta>
 cudaError_t dtq_launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB,
@@ -60,13 +60,19 @@ cudaError_t dtq_launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB,
   cfg.blockDim = dim3(dtq_gemm::num_threads<BN, kW4>());
   cfg.dynamicSmemBytes = L::alloc;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = per;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // programmatic dependent launch: the GEMM's CTAs may start (barrier init,
+  // TMEM allocation, descriptor prefetch) while the quantizer that produces
+  // its A operand drains; the kernel waits (griddepcontrol.wait) before
+  // touching codes / s_x / z_x
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, tA, tB, tY, g);
 }
 

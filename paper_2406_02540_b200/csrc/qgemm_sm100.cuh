@@ -71,7 +71,7 @@ struct Smem {
   static constexpr int kA = BM * BK;                   // 16 KB (this CTA's 128 rows)
   static constexpr int kBRows = k2Cta ? BN / 2 : BN;   // a CTA pair splits B along N
   static constexpr int kB = kBRows * BK;               // s8 tile
-  static constexpr int kP = kW4 ? BN * (BK / 2) : 0;   // packed nibbles
+  static constexpr int kP = kW4 ? kBRows * (BK / 2) : 0;  // packed nibbles (this CTA's rows)
   static constexpr int kEpiBufs = 2;                             // staging buffers per warp
   static constexpr int kEpi = epi_warps<kW4>() * kEpiBufs * 32 * 64;  // 32 rows x 64 B each
   static constexpr int kPar = 2 * 3 * BN * 4;             // {s_w, wsum, bias} x 2 tiles
@@ -92,20 +92,16 @@ __host__ __device__ constexpr int num_threads() {
   return 32 * (2 + epi_warps<kW4>() + (kW4 ? kConvWarps : 0));
 }
 
-__device__ __forceinline__ uint32_t s4x8_to_s8x8_lo(uint32_t w) {
-  // 8 LSB-first nibbles (codes, z = 8) -> bytes of (code - 8) for elements 0..3
-  const uint32_t lo = w & 0x0F0F0F0Fu;         // elements 0, 2, 4, 6
-  const uint32_t hi = (w >> 4) & 0x0F0F0F0Fu;  // elements 1, 3, 5, 7
-  uint32_t e = __byte_perm(lo, hi, 0x5140);    // e0 e1 e2 e3
-  e ^= 0x08080808u;                            // code - 8 as 4-bit two's complement
-  return e | ((e & 0x08080808u) * 0x1Eu);      // sign-extend to 8 bits
-}
-__device__ __forceinline__ uint32_t s4x8_to_s8x8_hi(uint32_t w) {
-  const uint32_t lo = w & 0x0F0F0F0Fu;
-  const uint32_t hi = (w >> 4) & 0x0F0F0F0Fu;
-  uint32_t e = __byte_perm(lo, hi, 0x7362);    // e4 e5 e6 e7
-  e ^= 0x08080808u;
-  return e | ((e & 0x08080808u) * 0x1Eu);
+// 8 LSB-first nibbles (trace_io.cpp:79-91 order; codes c, z_w = 8) -> 8 bytes
+// holding 16*(c - 8) as s8: the nibble (c ^ 8) is the 4-bit two's complement
+// of c - 8, and placed in the HIGH half of a byte it is exactly 16*(c - 8).
+// Five instructions per 8 weights; the GEMM folds the factor 16 back out
+// exactly (s_x/16 in the dequant, 16*sum(w) in the zero-point term, >>4 for
+// the raw accumulator).
+__device__ __forceinline__ uint2 s4x8_to_s8x8_x16(uint32_t w) {
+  const uint32_t hi = (w ^ 0x80808080u) & 0xF0F0F0F0u;         // odd elements
+  const uint32_t lo = ((w << 4) ^ 0x80808080u) & 0xF0F0F0F0u;  // even elements
+  return make_uint2(__byte_perm(lo, hi, 0x5140), __byte_perm(lo, hi, 0x7362));
 }
 
 // k2Cta: a cluster of two CTAs on one TPC computes a 256 x BN tile with
@@ -120,7 +116,6 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     qgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmY, const GemmArgs g) {
   using namespace dtq_ptx;
-  static_assert(!(kW4 && k2Cta), "W4A8 runs on the single-CTA kernel");
   using L = Smem<BN, kStages, kW4, k2Cta>;
   constexpr uint32_t kTmemCols = 2 * BN;
   constexpr int kTileM = k2Cta ? 2 * BM : BM;
@@ -174,7 +169,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&conv[s], kConvWarps);
+      mbar_init(&conv[s], kConvWarps * (k2Cta ? 2 : 1));  // leader's: both CTAs convert
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -195,6 +190,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // A codes, s_x, z_x come from the preceding quantizer kernel
 
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
@@ -206,7 +202,14 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         const int n0 = (tile / g.tiles_m) * BN;
         for (int kb = 0; kb < g.k_blocks; ++kb) {
           timed_wait(&empty[s], ph ^ 1, pw0);
-          if constexpr (k2Cta) {
+          if constexpr (k2Cta && kW4) {
+            // A of both CTAs lands on the leader's barrier; each CTA's packed
+            // nibbles land on its OWN barrier, which its converters wait on
+            const uint32_t lead_full = mapa_shared(smem_u32(&full[s]), 0);
+            mbar_arrive_expect_tx(&full[s], rank == 0 ? 2 * L::kA + L::kP : L::kP);
+            tma_load_2d_2sm(sA + s * L::kA, &tmA, lead_full, kb * BK, m0);
+            tma_load_2d(sP + s * L::kP, &tmB, &full[s], kb * (BK / 2), n0 + rank * L::kBRows);
+          } else if constexpr (k2Cta) {
             // both CTAs' bytes land on the leader's barrier; only it arms it
             const uint32_t lead_full = mapa_shared(smem_u32(&full[s]), 0);
             if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (L::kA + L::kB));
@@ -298,11 +301,12 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         const int col = tn0 + et + i * 32 * kEpiWarps;
         const bool okc = col < g.N && et + i * 32 * kEpiWarps < BN;
         p_sw[i] = __float_as_uint(okc ? __ldg(g.s_w + col) : 0.f);
-        p_ws[i] = static_cast<uint32_t>(okc ? -__ldg(g.wsum + col) : 0);
+        // W4: the unpacked weights are 16*w (s4x8_to_s8x8_x16), so is their sum
+        p_ws[i] = static_cast<uint32_t>(okc ? -__ldg(g.wsum + col) * (kW4 ? 16 : 1) : 0);
         p_b[i] = __float_as_uint((okc && g.bias) ? __ldg(g.bias + col) : 0.f);
       }
       const int row = tm0 + q * 32 + lane;
-      nsx = row < g.M ? static_cast<float>(__ldg(g.s_x + row)) : 0.f;
+      nsx = row < g.M ? static_cast<float>(__ldg(g.s_x + row)) * (kW4 ? 0.0625f : 1.f) : 0.f;
       nzx = row < g.M ? __ldg(g.z_x + row) : 0;
     };
     if (tile0 < total_tiles) fetch(tile0);
@@ -401,7 +405,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
               for (int u = 0; u < 4; ++u) w[j4 + u] = __float_as_uint(f[u]);
             } else {
 #pragma unroll
-              for (int u = 0; u < 4; ++u) w[j4 + u] = static_cast<uint32_t>(a32[u]);
+              for (int u = 0; u < 4; ++u) w[j4 + u] = static_cast<uint32_t>(a32[u] >> (kW4 ? 4 : 0));
             }
           }
           if (g.dbg == 3) {  // diagnostics: keep the math alive, skip staging + stores
@@ -494,18 +498,23 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         mbar_wait(&full[s], ph);
         const uint8_t* src = sP + s * L::kP;
         uint8_t* dst = sB + s * L::kB;
-        // BN rows x 8 granules of 16 output bytes (= 8 packed bytes each)
+        // this CTA's B rows x 8 granules of 16 output bytes (= 8 packed bytes each)
 #pragma unroll 4
-        for (int item = ct; item < BN * 8; item += 32 * kConvWarps) {
+        for (int item = ct; item < L::kBRows * 8; item += 32 * kConvWarps) {
           const int r = item >> 3, j = item & 7;
           const uint2 w = *reinterpret_cast<const uint2*>(src + r * 64 + j * 8);
-          const uint4 o = make_uint4(s4x8_to_s8x8_lo(w.x), s4x8_to_s8x8_hi(w.x),
-                                     s4x8_to_s8x8_lo(w.y), s4x8_to_s8x8_hi(w.y));
+          const uint2 o0 = s4x8_to_s8x8_x16(w.x), o1 = s4x8_to_s8x8_x16(w.y);
+          const uint4 o = make_uint4(o0.x, o0.y, o1.x, o1.y);
           *reinterpret_cast<uint4*>(dst + r * 128 + ((j ^ (r & 7)) * 16)) = o;
         }
         fence_proxy_async_smem();  // generic-proxy writes -> visible to the MMA (async proxy)
         __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[s]);
+        if (lane == 0) {
+          if constexpr (k2Cta)  // the leader's MMA reads both CTAs' B halves
+            mbar_arrive_cluster_release(mapa_shared(smem_u32(&conv[s]), 0));
+          else
+            mbar_arrive(&conv[s]);
+        }
         if (++s == kStages) {
           s = 0;
           ph ^= 1;

@@ -306,3 +306,21 @@ def test_deterministic():
     y1 = layer.forward(x)
     y2 = layer.forward(x)
     assert torch.equal(y1, y2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("wcode", [0, 15])
+def test_w4_extreme_codes_exact(wcode):
+    # W4 weights enter the MMA as 16*(c - 8): the extremes (-128, +112 as s8)
+    # at the largest STDiT K must still give the exact int32 accumulator
+    K, N, M = 4608, 256, 512
+    codes = torch.full((N, K), wcode, dtype=torch.uint8, device=DEV)
+    layer = dtq.QuantLinear.from_codes(codes, torch.ones(N, dtype=torch.float64, device=DEV), 4, K)
+    a = torch.full((M, K), 255, dtype=torch.uint8, device=DEV)
+    a[1::2] = 0
+    z = torch.zeros(M, dtype=torch.int32, device=DEV)
+    z[2::4] = 255
+    acc = layer.gemm(a, torch.ones(M, dtype=torch.float64, device=DEV), z, out_dtype=torch.int32)
+    x = a.cpu().long() - z.cpu().long()[:, None]
+    want = x.sum(1, keepdim=True) * (wcode - 8)
+    assert torch.equal(acc.cpu().long(), want.expand(M, N))

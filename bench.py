@@ -444,6 +444,20 @@ def run_ours(args, world, rank, local):
     except Exception:
         t_i8 = None
 
+    # multi-GPU verification, outside the timed region: every rank ran the same
+    # per-rank workload, so the all-gathered output checksums must agree
+    # (NCCL all_gather over NVLink; shard.py holds the row-sharded variant)
+    verify = None
+    if world > 1:
+        import torch.distributed as dist
+        layer.forward(x, out=y, workspace=ws)
+        ck = torch.stack([y.double().sum(), y.double().abs().sum(),
+                          codes.double().sum()]).to(dev)
+        parts = [torch.empty_like(ck) for _ in range(world)]
+        dist.all_gather(parts, ck)
+        same = all(bool(torch.equal(p, parts[0])) for p in parts)
+        verify = {"ranks": world, "outputs_identical": same, "collective": "nccl all_gather",
+                  "timed": False}
     stack = None
     if not args.no_stack:
         try:
@@ -507,6 +521,7 @@ def run_ours(args, world, rank, local):
                 "h2d_bytes_per_step": 2 * M * K, "d2h_bytes_per_step": 2 * M * N,
                 "ms": t_e2e * 1e3, "api": "dtq_qlinear_forward_host"},
         "stack": stack,
+        "multi_gpu_verify": verify,
         "gpu_launches": 2 * args.steps,   # fused quantizer + GEMM per timed step
         "clocks": clk.summary(),
         "cpu_baseline": cpu,

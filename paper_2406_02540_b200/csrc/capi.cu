@@ -232,6 +232,11 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
   a.pro = kind;
   a.smooth_mul = smooth_mul;
   a.probe = fq_probe_buffer();
+  static const int fq_dbg = [] {
+    const char* e = std::getenv("DTQ_DEBUG_FQ");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.dbg = fq_dbg;
   const int sms = device_info().sms;
 
   // the fp32 kernel needs 16-byte rows, K % 128 == 0 and a 128-column
@@ -415,6 +420,12 @@ struct dtq_qlinear_s {
   void* hy = nullptr;
   size_t hy_bytes = 0;
   int32_t* status = nullptr;
+  // host-forward pipeline: two streams alternate row chunks (H2D, quantize +
+  // GEMM, D2H), each with its own workspace
+  cudaStream_t ps[2] = {nullptr, nullptr};
+  cudaEvent_t pe[3] = {nullptr, nullptr, nullptr};
+  void* pws[2] = {nullptr, nullptr};
+  size_t pws_bytes[2] = {0, 0};
 };
 
 namespace {
@@ -434,6 +445,12 @@ void free_handle(dtq_qlinear_s* h) {
                   h->col_mul, h->signs, h->scratch, h->acc32, h->hx, h->hy, h->status};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (int i = 0; i < 2; ++i) {
+    if (h->pws[i]) cudaFree(h->pws[i]);
+    if (h->ps[i]) cudaStreamDestroy(h->ps[i]);
+  }
+  for (cudaEvent_t e : h->pe)
+    if (e) cudaEventDestroy(e);
   delete h;
 }
 
@@ -908,17 +925,58 @@ int dtq_qlinear_quantize(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq
 int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_t h, int mode,
                              void* y, int y_dtype, void* stream) {
   if (!h || !x || !y || M <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "forward_host: bad args");
-  const size_t xb = dtype_size(x_dtype) * static_cast<size_t>(M) * h->K;
-  const size_t yb = dtype_size(y_dtype) * static_cast<size_t>(M) * h->N;
+  const size_t xe = dtype_size(x_dtype), ye = dtype_size(y_dtype);
+  const size_t xb = xe * static_cast<size_t>(M) * h->K;
+  const size_t yb = ye * static_cast<size_t>(M) * h->N;
   if (xb == 0 || yb == 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "forward_host: bad dtype");
   cudaStream_t st = as_stream(stream);
   DTQ_TRY(grow(&h->hx, &h->hx_bytes, xb));
   DTQ_TRY(grow(&h->hy, &h->hy_bytes, yb));
   CUDA_TRY(cudaMemsetAsync(h->status, 0, sizeof(int32_t), st));
-  CUDA_TRY(cudaMemcpyAsync(h->hx, x, xb, cudaMemcpyHostToDevice, st));
-  DTQ_TRY(forward_impl(h->hx, x_dtype, M, h->K, h, mode, nullptr, h->hy, y_dtype, h->N, nullptr,
-                       0, h->status, st));
-  CUDA_TRY(cudaMemcpyAsync(y, h->hy, yb, cudaMemcpyDeviceToHost, st));
+  // Row chunks (>= 256 rows, ~8 of them) pipelined over two streams so the
+  // H2D of chunk i+1 and the D2H of chunk i-1 overlap chunk i's kernels
+  // (quantization is row-local, so chunks are independent).  The F64 parity
+  // output uses a handle-wide s32 scratch and stays in one piece.
+  int64_t chunk = (M + 7) / 8;
+  chunk = (chunk + 255) / 256 * 256;
+  if (y_dtype == DTQ_F64 || M < 1024) chunk = M;
+  if (chunk >= M) {
+    CUDA_TRY(cudaMemcpyAsync(h->hx, x, xb, cudaMemcpyHostToDevice, st));
+    DTQ_TRY(forward_impl(h->hx, x_dtype, M, h->K, h, mode, nullptr, h->hy, y_dtype, h->N,
+                         nullptr, 0, h->status, st));
+    CUDA_TRY(cudaMemcpyAsync(y, h->hy, yb, cudaMemcpyDeviceToHost, st));
+  } else {
+    int64_t ldc;
+    size_t a_, b_;
+    const size_t wsb = ws_layout(h, chunk, &ldc, &a_, &b_);
+    for (int i = 0; i < 2; ++i) {
+      if (!h->ps[i]) CUDA_TRY(cudaStreamCreateWithFlags(&h->ps[i], cudaStreamNonBlocking));
+      DTQ_TRY(grow(&h->pws[i], &h->pws_bytes[i], wsb));
+    }
+    for (int i = 0; i < 3; ++i)
+      if (!h->pe[i]) CUDA_TRY(cudaEventCreateWithFlags(&h->pe[i], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(h->pe[0], st));
+    CUDA_TRY(cudaStreamWaitEvent(h->ps[0], h->pe[0], 0));
+    CUDA_TRY(cudaStreamWaitEvent(h->ps[1], h->pe[0], 0));
+    int c = 0;
+    for (int64_t r0 = 0; r0 < M; r0 += chunk, ++c) {
+      const int64_t m = M - r0 < chunk ? M - r0 : chunk;
+      cudaStream_t s = h->ps[c & 1];
+      const size_t xo = xe * static_cast<size_t>(r0) * h->K, yo = ye * static_cast<size_t>(r0) * h->N;
+      uint8_t* dx = static_cast<uint8_t*>(h->hx) + xo;
+      uint8_t* dy = static_cast<uint8_t*>(h->hy) + yo;
+      CUDA_TRY(cudaMemcpyAsync(dx, static_cast<const uint8_t*>(x) + xo, xe * m * h->K,
+                               cudaMemcpyHostToDevice, s));
+      DTQ_TRY(forward_impl(dx, x_dtype, m, h->K, h, mode, nullptr, dy, y_dtype, h->N,
+                           h->pws[c & 1], h->pws_bytes[c & 1], h->status, s));
+      CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(y) + yo, dy, ye * m * h->N,
+                               cudaMemcpyDeviceToHost, s));
+    }
+    CUDA_TRY(cudaEventRecord(h->pe[1], h->ps[0]));
+    CUDA_TRY(cudaEventRecord(h->pe[2], h->ps[1]));
+    CUDA_TRY(cudaStreamWaitEvent(st, h->pe[1], 0));
+    CUDA_TRY(cudaStreamWaitEvent(st, h->pe[2], 0));
+  }
   int32_t bad = 0;
   CUDA_TRY(cudaMemcpyAsync(&bad, h->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));

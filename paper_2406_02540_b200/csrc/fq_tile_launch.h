@@ -1,0 +1,53 @@
+// fq_tile_launch.h -- launcher template of the tile quantizer, shared by the
+// per-dtype translation units (fq_tile.cu, fq_tile_f16.cu, fq_tile_bf16.cu).
+#pragma once
+#include <cstdlib>
+
+#include "fused_quant_tile.cuh"
+
+namespace {  // NOLINT
+
+template <typename Tin, bool kRot, bool kExactV, int kPro>
+cudaError_t launch_tile(const dtq_fq::FqArgs& a, int R, int sms, cudaStream_t st) {
+  const bool wide = dtq_fq::fq_lanes(a.K) == 2;  // K > 2304: two lanes per block, 576 threads
+  auto kern = wide ? dtq_fq::fq_tile_kernel<Tin, kRot, kExactV, kPro, true>
+                   : dtq_fq::fq_tile_kernel<Tin, kRot, kExactV, kPro, false>;
+  const bool has_b = a.pro == dtq_fq::kProModulate || a.pro == dtq_fq::kProLnModulate;
+  const bool has_a = has_b || a.col_mul != nullptr;
+  const dtq_fq::TileLayout L = dtq_fq::fq_tile_layout(a.K, R, sizeof(Tin), has_a, has_b);
+  const int nb = static_cast<int>(a.K / 128);
+  const int block = dtq_fq::fq_tile_threads(a.K, R);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(L.bytes));
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, L.bytes);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles = (a.M + R - 1) / R;
+  const int64_t cap = static_cast<int64_t>(sms) * (occ > 0 ? occ : 1);
+  const int grid = static_cast<int>(tiles < cap ? tiles : cap);
+  kern<<<grid, block, L.bytes, st>>>(a, R);
+  return cudaGetLastError();
+}
+
+template <typename Tin, int kPro>
+cudaError_t launch_p(const dtq_fq::FqArgs& a, bool rot, int R, int sms, cudaStream_t st) {
+  if (rot) return launch_tile<Tin, true, false, kPro>(a, R, sms, st);
+  if constexpr (kPro == dtq_fq::kProNone) {
+    // no prologue, smoothing or rotation: codes are reachable bit for bit
+    if (a.col_mul == nullptr) return launch_tile<Tin, false, true, kPro>(a, R, sms, st);
+  }
+  return launch_tile<Tin, false, false, kPro>(a, R, sms, st);
+}
+
+template <typename Tin>
+cudaError_t launch_rot(const dtq_fq::FqArgs& a, bool rot, int R, int sms, cudaStream_t st) {
+  switch (a.pro) {
+    case dtq_fq::kProModulate: return launch_p<Tin, dtq_fq::kProModulate>(a, rot, R, sms, st);
+    case dtq_fq::kProGelu: return launch_p<Tin, dtq_fq::kProGelu>(a, rot, R, sms, st);
+    case dtq_fq::kProLnModulate: return launch_p<Tin, dtq_fq::kProLnModulate>(a, rot, R, sms, st);
+    default: return launch_p<Tin, dtq_fq::kProNone>(a, rot, R, sms, st);
+  }
+}
+
+}  // namespace

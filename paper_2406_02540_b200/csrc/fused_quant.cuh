@@ -62,6 +62,7 @@ struct FqArgs {
   const float* col_mul;       // fast kernel: folded sign/s_c/sqrt(hblock) per column
   unsigned long long* probe;  // diagnostics: per-warp phase cycles (or nullptr)
   int tpr;                    // threads per row (multiple of 16 and of hblock/8)
+  int dbg;                    // diagnostics (tile kernel): 1 = skip the transform
 };
 
 // ------------------------------------------------------------------ GELU
@@ -72,28 +73,33 @@ struct FqArgs {
 // |error| <= 3e-7 absolute / 4e-6 relative overall (exp2 on the MUFU, one
 // per element; u is clamped at 1, where E < 2e-7 and decays faster than
 // the clamp's overestimate grows).  Coefficients below are -erfcx/2.
-__device__ __forceinline__ float2 gelu2(float2 x) {
-  const float2 ax = make_float2(fabsf(x.x), fabsf(x.y));
-  const float2 z = __fmul2_rn(ax, make_float2(0.70710678118654752f, 0.70710678118654752f));
-  float2 u = __ffma2_rn(z, make_float2(0.5555555555555556f, 0.5555555555555556f),
-                        make_float2(-1.f, -1.f));
-  u.x = fminf(u.x, 1.f);
-  u.y = fminf(u.y, 1.f);
-  constexpr float c[12] = {-1.392797530e-01f, 1.130055413e-01f,  -8.514883369e-02f,
-                           6.025094911e-02f,  -4.006979242e-02f, 2.551725321e-02f,
-                           -1.695104688e-02f, 1.010451838e-02f,  -2.978448523e-03f,
-                           1.512928284e-03f,  -3.386956872e-03f, 1.792096766e-03f};
-  float2 acc = make_float2(c[11], c[11]);
-#pragma unroll
-  for (int k = 10; k >= 0; --k) acc = __ffma2_rn(acc, u, make_float2(c[k], c[k]));
-  const float2 arg = __fmul2_rn(__fmul2_rn(z, z), make_float2(-1.4426950408889634f,
-                                                                -1.4426950408889634f));
-  float2 e;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(arg.x));
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(arg.y));
-  const float2 nE = __fmul2_rn(e, acc);  // -E
-  return __ffma2_rn(ax, nE, make_float2(fmaxf(x.x, 0.f), fmaxf(x.y, 0.f)));
+__device__ __forceinline__ float gelu_nerfcx_poly(float u) {
+  // Horner with literal coefficients: FFMA's immediate form (twice the issue
+  // rate of the 3-register form) and no coefficient registers
+  float a = 1.792096766e-03f;
+  a = fmaf(a, u, -3.386956872e-03f);
+  a = fmaf(a, u, 1.512928284e-03f);
+  a = fmaf(a, u, -2.978448523e-03f);
+  a = fmaf(a, u, 1.010451838e-02f);
+  a = fmaf(a, u, -1.695104688e-02f);
+  a = fmaf(a, u, 2.551725321e-02f);
+  a = fmaf(a, u, -4.006979242e-02f);
+  a = fmaf(a, u, 6.025094911e-02f);
+  a = fmaf(a, u, -8.514883369e-02f);
+  a = fmaf(a, u, 1.130055413e-01f);
+  return fmaf(a, u, -1.392797530e-01f);
 }
+
+__device__ __forceinline__ float gelu1(float x) {
+  const float ax = fabsf(x);
+  const float z = ax * 0.70710678118654752f;
+  const float u = fminf(fmaf(z, 0.5555555555555556f, -1.f), 1.f);
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(z * z * -1.4426950408889634f));
+  return fmaf(ax, e * gelu_nerfcx_poly(u), fmaxf(x, 0.f));  // max(x,0) - |x| E
+}
+
+__device__ __forceinline__ float2 gelu2(float2 x) { return make_float2(gelu1(x.x), gelu1(x.y)); }
 
 // ------------------------------------------------------------------ loads
 template <typename T>

@@ -45,6 +45,18 @@
 
 namespace dtq_fq {
 
+// Lanes per 128-column block: kQ = 4 for K <= 2304 (32 values per lane,
+// <= 72 registers, three 288-thread CTAs per SM), kQ = 2 for wider rows (64
+// values per lane, 576-thread CTAs).  Derived per-lane shapes:
+template <int kQ>
+struct FqShape {
+  static constexpr int kE = 128 / kQ;      // values per lane
+  static constexpr int kPairs = kE / 2;    // fp32 pairs
+  static constexpr int kRuns = kE / 16;    // 16-column runs
+  static constexpr int kItems = 32 / kQ;   // (row, block) items per warp
+};
+__host__ __device__ constexpr int fq_lanes(int64_t K) { return K <= 2304 ? 4 : 2; }
+
 struct TileLayout {
   size_t pitch_in;
   size_t off_in1, off_a, off_b, off_red, off_bar, bytes;
@@ -67,7 +79,7 @@ __host__ __device__ inline TileLayout fq_tile_layout(int64_t K, int R, int es, b
 }
 
 __host__ __device__ inline int fq_tile_threads(int64_t K, int R) {
-  return static_cast<int>((2 * R * (K / 128) + 31) / 32 * 32);
+  return static_cast<int>((fq_lanes(K) * R * (K / 128) + 31) / 32 * 32);
 }
 
 __device__ __forceinline__ float max3f(float a, float b, float c) {
@@ -85,10 +97,11 @@ constexpr float kFqTie = 0.5f - 3.0517578125e-05f;  // 1/2 - 2^-15
 
 // Exact re-evaluation (quant.cpp:169-175 in fp64) of the flagged 16-value
 // runs of one lane: v[16m + i] is run m, w[4m .. 4m+3] its packed codes.
-__device__ __noinline__ void fq_tile_fix(const float* v, uint32_t* w, unsigned runs, float inv_sf,
-                                         float zm, double s, double z, double qmax) {
+static __device__ __noinline__ void fq_tile_fix(const float* v, uint32_t* w, int nruns,
+                                                unsigned runs, float inv_sf, float zm, double s,
+                                                double z, double qmax) {
 #pragma unroll 1
-  for (int m = 0; m < 4; ++m) {
+  for (int m = 0; m < nruns; ++m) {
     if (!((runs >> m) & 1u)) continue;
 #pragma unroll 1
     for (int i = 0; i < 16; ++i) {
@@ -125,23 +138,28 @@ __device__ __forceinline__ void ld16(const uint8_t* p, float (&o)[16]) {
   }
 }
 
-// value l (0..63) of a lane: P[l & 31].x for l < 32, .y otherwise
-#define FQ_V(P, l) ((l) < 32 ? (P)[(l)&31].x : (P)[(l)&31].y)
+// value l (0..kE-1) of a lane: P[l % kPairs].x for l < kPairs, .y otherwise
+#define FQ_V(P, l) ((l) < S::kPairs ? (P)[(l) % S::kPairs].x : (P)[(l) % S::kPairs].y)
 
-// 64 codes of one lane -> 4 x 16-byte stores (runs m = 0..3)
-template <bool kClamp, bool kExactV>
-__device__ __forceinline__ void fq_tile_codes(const float2 (&P)[32], float inv_sf, float zm,
+// kE codes of one lane -> one 16-byte store per run (run m at dst + 16*kQ*m)
+template <int kQ, bool kClamp, bool kExactV>
+__device__ __forceinline__ void fq_tile_codes(const float2 (&P)[FqShape<kQ>::kPairs], float inv_sf,
+                                              float zm,
                                               int qmax_i, double s, double z, double qmax,
                                               uint8_t* __restrict__ dst) {
   const float2 inv2 = make_float2(inv_sf, inv_sf), zm2 = make_float2(zm, zm);
   const float2 neg = make_float2(-1.f, -1.f);
   const float lo = 12582912.0f, hi = 12582912.0f + static_cast<float>(qmax_i);
-  uint32_t w[16];   // run m (values 16m..16m+15) -> w[4m..4m+3]
-  float em[4] = {0.f, 0.f, 0.f, 0.f};
+  using S = FqShape<kQ>;
+  constexpr int kHalf = S::kRuns / 2;
+  uint32_t w[4 * S::kRuns];  // run m (values 16m..16m+15) -> w[4m..4m+3]
+  float em[S::kRuns];
 #pragma unroll
-  for (int g = 0; g < 4; ++g) {  // pairs 4g..4g+3 of each 16-pair half
+  for (int m = 0; m < S::kRuns; ++m) em[m] = 0.f;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+  for (int g = 0; g < 4; ++g) {  // pairs 4g..4g+3 of each 16-pair group
+#pragma unroll
+    for (int h = 0; h < kHalf; ++h) {
       uint32_t cx[4], cy[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -150,7 +168,7 @@ __device__ __forceinline__ void fq_tile_codes(const float2 (&P)[32], float inv_s
         if constexpr (kExactV) {
           const float2 e = __ffma2_rn(v, inv2, __ffma2_rn(rr, neg, zm2));  // exact residual
           em[h] = fmaxf(em[h], fabsf(e.x));
-          em[2 + h] = fmaxf(em[2 + h], fabsf(e.y));
+          em[kHalf + h] = fmaxf(em[kHalf + h], fabsf(e.y));
         }
         if constexpr (kClamp) {
           rr.x = fminf(fmaxf(rr.x, lo), hi);
@@ -159,32 +177,39 @@ __device__ __forceinline__ void fq_tile_codes(const float2 (&P)[32], float inv_s
         cx[u] = __float_as_uint(rr.x);
         cy[u] = __float_as_uint(rr.y);
       }
-      // .x of pairs 16h + .. -> run h; .y -> run 2 + h
+      // .x of pairs 16h + .. -> run h; .y -> run kHalf + h
       w[4 * h + g] = __byte_perm(__byte_perm(cx[0], cx[1], 0x0040),
                                  __byte_perm(cx[2], cx[3], 0x0040), 0x5410);
-      w[4 * (2 + h) + g] = __byte_perm(__byte_perm(cy[0], cy[1], 0x0040),
-                                       __byte_perm(cy[2], cy[3], 0x0040), 0x5410);
+      w[4 * (kHalf + h) + g] = __byte_perm(__byte_perm(cy[0], cy[1], 0x0040),
+                                           __byte_perm(cy[2], cy[3], 0x0040), 0x5410);
     }
   }
   if constexpr (kExactV) {
-    const unsigned runs = (em[0] > kFqTie ? 1u : 0u) | (em[1] > kFqTie ? 2u : 0u) |
-                          (em[2] > kFqTie ? 4u : 0u) | (em[3] > kFqTie ? 8u : 0u);
+    unsigned runs = 0;
+#pragma unroll
+    for (int m = 0; m < S::kRuns; ++m) runs |= (em[m] > kFqTie ? 1u : 0u) << m;
     if (runs) {
       // copy out (keeps P itself in registers) and re-evaluate exactly
-      float vb[64];
+      float vb[S::kE];
 #pragma unroll
-      for (int l = 0; l < 64; ++l) vb[l] = FQ_V(P, l);
-      fq_tile_fix(vb, w, runs, inv_sf, zm, s, z, qmax);
+      for (int l = 0; l < S::kE; ++l) vb[l] = FQ_V(P, l);
+      fq_tile_fix(vb, w, S::kRuns, runs, inv_sf, zm, s, z, qmax);
     }
   }
 #pragma unroll
-  for (int m = 0; m < 4; ++m)
-    *reinterpret_cast<uint4*>(dst + 32 * m) = make_uint4(w[4 * m], w[4 * m + 1], w[4 * m + 2],
-                                                         w[4 * m + 3]);
+  for (int m = 0; m < S::kRuns; ++m)
+    *reinterpret_cast<uint4*>(dst + 16 * kQ * m) =
+        make_uint4(w[4 * m], w[4 * m + 1], w[4 * m + 2], w[4 * m + 3]);
 }
 
-template <typename Tin, bool kRot, bool kExactV, int kPro>
-__global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const int R) {
+// kWide: 576-thread CTAs (K > 2304, one per SM); otherwise <= 288 threads
+// with registers capped for three CTAs per SM
+template <typename Tin, bool kRot, bool kExactV, int kPro, bool kWide>
+__global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
+    fq_tile_kernel(const FqArgs a, const int R) {
+  constexpr int kFqQ = kWide ? 2 : 4;
+  using S = FqShape<kFqQ>;
+  constexpr int kFqE = S::kE, kFqPairs = S::kPairs, kFqRuns = S::kRuns, kFqItems = S::kItems;
   extern __shared__ __align__(128) uint8_t fq_smem[];
   constexpr int es = sizeof(Tin);
   constexpr bool has_b = kPro == kProModulate || kPro == kProLnModulate;
@@ -192,8 +217,8 @@ __global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const i
   const int nb = K >> 7;
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
-  const int p = lane >> 4;
-  const int q = warp * 16 + (lane & 15);  // (row, block) pair index
+  const int p = lane / kFqItems;                         // lane's part of its block
+  const int q = warp * kFqItems + (lane % kFqItems);    // (row, block) item index
   const int r = q & (R - 1);
   const int b_raw = q / R;
   const bool active = b_raw < nb;  // blockDim is rounded up to whole warps
@@ -268,9 +293,18 @@ __global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const i
   __syncthreads();
   const int qmax_i = (1 << a.bits) - 1;
   const double qmax = static_cast<double>(qmax_i);
-  const float sg16 = p ? -1.f : 1.f;
-  const int c0 = b * 128 + 16 * p;  // first column of run 0
+  const float sg16 = (p & 1) ? -1.f : 1.f;
+  const float sg32 = (p & 2) ? -1.f : 1.f;
+  const int c0 = b * 128 + 16 * p;  // first column of run 0; run m at + 16*kFqQ*m
 
+  // diagnostics (built with -DFQ_TILE_PROBE, DTQ_DEBUG_FQ_PROBE=1): per-CTA
+  // cycles in data waits, in the tile barrier and in total (warp 1, lane 0)
+#ifdef FQ_TILE_PROBE
+  const bool probe = a.probe != nullptr && t == 32;
+#else
+  constexpr bool probe = false;
+#endif
+  long long pr_t0 = probe ? clock64() : 0, pr_wait = 0, pr_bar = 0;
   for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
     const int buf = it & 1;
     const int64_t row = tile * R + r;
@@ -280,17 +314,22 @@ __global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const i
       dtq_ptx::fence_proxy_async_smem();
       issue(tile + gridDim.x, buf ^ 1);
     }
-    dtq_ptx::mbar_wait(bar + buf, (it >> 1) & 1);
+    {
+      const long long w0 = probe ? clock64() : 0;
+      dtq_ptx::mbar_wait(bar + buf, (it >> 1) & 1);
+      if (probe) pr_wait += clock64() - w0;
+    }
 
-    // ---- 1. own 64 values -> registers: run m = columns c0 + 32m + 0..15
-    float2 P[32];
+    // ---- 1. own kFqE values -> registers: run m = columns c0 + 16*kFqQ*m + 0..15;
+    // runs m < kFqRuns/2 fill P[16m + i].x, the others .y
+    float2 P[kFqPairs];
     {
       const uint8_t* src = fq_smem + buf * L.off_in1 + r * L.pitch_in + c0 * es;
 #pragma unroll
-      for (int m = 0; m < 2; ++m) {
+      for (int m = 0; m < kFqRuns / 2; ++m) {
         float lo[16], hi[16];
-        ld16<Tin>(src + 32 * m * es, lo);
-        ld16<Tin>(src + 32 * (m + 2) * es, hi);
+        ld16<Tin>(src + 16 * kFqQ * m * es, lo);
+        ld16<Tin>(src + (16 * kFqQ * m + 64) * es, hi);
 #pragma unroll
         for (int i = 0; i < 16; ++i) P[16 * m + i] = make_float2(lo[i], hi[i]);
       }
@@ -299,13 +338,14 @@ __global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const i
     // ---- 2. prologue
     if constexpr (kPro == kProGelu) {
 #pragma unroll
-      for (int k = 0; k < 32; ++k) P[k] = gelu2(P[k]);
+      for (int k = 0; k < kFqPairs; ++k) P[k] = gelu2(P[k]);
     } else if constexpr (kPro == kProLnModulate) {
       float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int k = 0; k < 32; ++k) s2 = __fadd2_rn(s2, P[k]);
+      for (int k = 0; k < kFqPairs; ++k) s2 = __fadd2_rn(s2, P[k]);
       float s1 = s2.x + s2.y;
-      s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+#pragma unroll
+      for (int o = kFqItems; o < 32; o <<= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, o);
       if (p == 0 && active) red_s1[b * R + r] = s1;
       __syncthreads();
       float tot = 0.f;
@@ -314,12 +354,13 @@ __global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const i
       const float2 nm = make_float2(-mean, -mean);
       float2 qq = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
+      for (int k = 0; k < kFqPairs; ++k) {
         const float2 d = __fadd2_rn(P[k], nm);
         qq = __ffma2_rn(d, d, qq);
       }
       float q1 = qq.x + qq.y;
-      q1 += __shfl_xor_sync(0xffffffffu, q1, 16);
+#pragma unroll
+      for (int o = kFqItems; o < 32; o <<= 1) q1 += __shfl_xor_sync(0xffffffffu, q1, o);
       if (p == 0 && active) red_s2[b * R + r] = q1;
       __syncthreads();
       float tq = 0.f;
@@ -327,16 +368,16 @@ __global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const i
       const float rstd = rsqrtf(tq / static_cast<float>(K) + a.eps);
       const float2 r2 = make_float2(rstd, rstd), o2 = make_float2(-mean * rstd, -mean * rstd);
 #pragma unroll
-      for (int k = 0; k < 32; ++k) P[k] = __ffma2_rn(P[k], r2, o2);
+      for (int k = 0; k < kFqPairs; ++k) P[k] = __ffma2_rn(P[k], r2, o2);
     }
 
     // ---- 3. folded column map, then the transform
     if (has_a) {
 #pragma unroll
-      for (int m = 0; m < 2; ++m) {
+      for (int m = 0; m < kFqRuns / 2; ++m) {
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          const int cl = c0 + 32 * m + 4 * g, ch = cl + 64;  // runs m and m + 2
+          const int cl = c0 + 16 * kFqQ * m + 4 * g, ch = cl + 64;  // .x run and .y run
           const float4 A0 = *reinterpret_cast<const float4*>(colA + cl);
           const float4 A1 = *reinterpret_cast<const float4*>(colA + ch);
           float2* Q = P + 16 * m + 4 * g;
@@ -356,11 +397,11 @@ __global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const i
         }
       }
     }
-    if constexpr (kRot) {
+    if (kRot && a.dbg != 1) {
       const float2 neg = make_float2(-1.f, -1.f);
       auto stage = [&](int h) {  // local stride h over the pair index
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
+        for (int k = 0; k < kFqPairs; ++k)
           if ((k & h) == 0) {
             const float2 sm = __fadd2_rn(P[k], P[k + h]);
             const float2 df = __ffma2_rn(P[k + h], neg, P[k]);
@@ -372,18 +413,22 @@ __global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const i
       stage(2);  // 2
       stage(4);  // 4
       stage(8);  // 8
-      {          // element stride 16: across the lane pair
-        const float2 sg = make_float2(sg16, sg16);
+      auto xlane = [&](int o, float sgn) {  // element stride 16 / 32 across lanes
+        const float2 sg = make_float2(sgn, sgn);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const float ox = __shfl_xor_sync(0xffffffffu, P[k].x, 16);
-          const float oy = __shfl_xor_sync(0xffffffffu, P[k].y, 16);
+        for (int k = 0; k < kFqPairs; ++k) {
+          const float ox = __shfl_xor_sync(0xffffffffu, P[k].x, o);
+          const float oy = __shfl_xor_sync(0xffffffffu, P[k].y, o);
           P[k] = __ffma2_rn(P[k], sg, make_float2(ox, oy));
         }
-      }
-      stage(16);  // element stride 32
+      };
+      xlane(kFqItems, sg16);  // element stride 16
+      if constexpr (kFqQ == 4)
+        xlane(2 * kFqItems, sg32);  // element stride 32
+      else
+        stage(16);  // element stride 32 (local stride 16)
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {  // element stride 64: inside each pair
+      for (int k = 0; k < kFqPairs; ++k) {  // element stride 64: inside each pair
         const float u = P[k].x, w = P[k].y;
         P[k] = make_float2(u + w, u - w);
       }
@@ -397,22 +442,25 @@ __global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const i
       } else {
         float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) s2 = __fadd2_rn(s2, P[k]);
+        for (int k = 0; k < kFqPairs; ++k) s2 = __fadd2_rn(s2, P[k]);
         sum = s2.x + s2.y;
       }
       if (!isfinite(sum)) {
         bool bad = false;
 #pragma unroll
-        for (int k = 0; k < 32; ++k) bad |= !isfinite(P[k].x) || !isfinite(P[k].y);
+        for (int k = 0; k < kFqPairs; ++k) bad |= !isfinite(P[k].x) || !isfinite(P[k].y);
         if (bad) atomicOr(a.status, 1);
       }
     }
 
     // ---- 4. row min / max -> params (fp64, quant.cpp:90-124)
     {
+      constexpr int kG = kFqPairs / 8;
       float mn4[4], mx4[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 4; ++i) mn4[i] = __int_as_float(0x7f800000), mx4[i] = -mn4[i];
+#pragma unroll
+      for (int i = 0; i < kG; ++i) {
         mn4[i] = fminf(P[8 * i].x, P[8 * i].y);
         mx4[i] = fmaxf(P[8 * i].x, P[8 * i].y);
 #pragma unroll
@@ -423,11 +471,18 @@ __global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const i
       }
       float mn = fminf(min3f(mn4[0], mn4[1], mn4[2]), mn4[3]);
       float mx = fmaxf(max3f(mx4[0], mx4[1], mx4[2]), mx4[3]);
-      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 16));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+#pragma unroll
+      for (int o = kFqItems; o < 32; o <<= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
       if (p == 0 && active) red_mm[(buf * nb + b) * R + r] = make_float2(mn, mx);
     }
-    __syncthreads();  // the one barrier per tile (also frees the input buffer)
+    {
+      const long long b0 = probe ? clock64() : 0;
+      __syncthreads();  // the one barrier per tile (also frees the input buffer)
+      if (probe) pr_bar += clock64() - b0;
+    }
     if (!ok) continue;
     float mn = __int_as_float(0x7f800000), mx = -mn;
     for (int j = 0; j < nb; ++j) {
@@ -484,9 +539,15 @@ __global__ void __launch_bounds__(576, 1) fq_tile_kernel(const FqArgs a, const i
     // ---- 5. codes straight from registers
     uint8_t* dst = a.codes + row * a.ldc + c0;
     if (clamp)
-      fq_tile_codes<true, kExactV>(P, inv_sf, zm, qmax_i, s, z, qmax, dst);
+      fq_tile_codes<kFqQ, true, kExactV>(P, inv_sf, zm, qmax_i, s, z, qmax, dst);
     else
-      fq_tile_codes<false, kExactV>(P, inv_sf, zm, qmax_i, s, z, qmax, dst);
+      fq_tile_codes<kFqQ, false, kExactV>(P, inv_sf, zm, qmax_i, s, z, qmax, dst);
+  }
+  if (probe) {
+    unsigned long long* pr = a.probe + blockIdx.x * 4;
+    pr[0] = static_cast<unsigned long long>(pr_wait);
+    pr[1] = static_cast<unsigned long long>(pr_bar);
+    pr[2] = static_cast<unsigned long long>(clock64() - pr_t0);
   }
 }
 

@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     constexpr int kPieceCols = 64 / esize;             // columns per 64-byte staged row
     int buf = 0;
     int it = 0;
+    const bool has_bias = g.bias != nullptr;
     // Per-column {s_w, -wsum, bias} and per-row {s_x, z_x} of the NEXT tile are
     // fetched into registers while the current tile is processed, then parked
     // in a double-buffered smem table: their global latency never stalls the
@@ -367,7 +368,10 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
             const int cc = c * 32 + piece * kPieceCols + j4;
             const uint4 sw4 = *reinterpret_cast<const uint4*>(par + cc);
             const uint4 ws4 = *reinterpret_cast<const uint4*>(par + BN + cc);
-            const uint4 b4 = *reinterpret_cast<const uint4*>(par + 2 * BN + cc);
+            // (no bias: skip the load -- the epilogue shares smem bandwidth with
+            // the MMA operand reads and the TMA ring)
+            const uint4 b4 = has_bias ? *reinterpret_cast<const uint4*>(par + 2 * BN + cc)
+                                      : make_uint4(0u, 0u, 0u, 0u);
             const uint32_t swv[4] = {sw4.x, sw4.y, sw4.z, sw4.w};
             const uint32_t wsv[4] = {ws4.x, ws4.y, ws4.z, ws4.w};
             const uint32_t bv[4] = {b4.x, b4.y, b4.z, b4.w};

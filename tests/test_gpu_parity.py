@@ -324,3 +324,21 @@ def test_w4_extreme_codes_exact(wcode):
     x = a.cpu().long() - z.cpu().long()[:, None]
     want = x.sum(1, keepdim=True) * (wcode - 8)
     assert torch.equal(acc.cpu().long(), want.expand(M, N))
+
+
+@pytest.mark.gpu
+def test_forward_host_pipelined_chunks_match_device_forward():
+    # M >= 1024 with a non-F64 output takes the chunked two-stream host
+    # pipeline; rows are independent, so it must equal the device forward
+    rng = np.random.default_rng(21)
+    M, K, N = 3000, 1152, 640
+    x = torch.from_numpy(activations(rng, M, K).astype(np.float16))
+    w = torch.from_numpy((rng.standard_normal((N, K)) / K ** 0.5).astype(np.float16))
+    signs = torch.from_numpy(dtq.hadamard_signs(K, 7)).to(DEV)
+    smooth = torch.from_numpy(rng.uniform(0.5, 2.0, K)).to(DEV)
+    layer = dtq.QuantLinear.create(w.to(DEV), 8, 8, balance=dtq.Balance(smooth, signs, 128))
+    want = layer.forward(x.to(DEV), out_dtype=torch.float16).cpu()
+    xh = x.pin_memory()
+    yh = torch.empty((M, N), dtype=torch.float16).pin_memory()
+    layer.forward_host(xh, yh)
+    assert torch.equal(yh, want)

@@ -558,6 +558,9 @@ GemmCfg choose_gemm_cfg(int64_t M, int64_t N, int wbits, int sms) {
   GemmCfg best{256, 0};
   int64_t best_cost = INT64_MAX;
   for (const GemmCfg& c : cands) {
+    // W4A8 is bound by the in-smem nibble unpack (smem bandwidth shared with
+    // the MMA operand reads): single-CTA tiles measure faster there
+    if (wbits == 4 && c.cta2) continue;
     const int64_t tm = c.cta2 ? 256 : 128;
     const int64_t tiles = ((M + tm - 1) / tm) * ((N + c.bn - 1) / c.bn);
     const int64_t units = c.cta2 ? sms / 2 : sms;

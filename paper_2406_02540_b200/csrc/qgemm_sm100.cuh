@@ -76,12 +76,16 @@ struct Smem {
   static constexpr int kEpi = epi_warps<kW4>() * kEpiBufs * 32 * 64;  // 32 rows x 64 B each
   static constexpr int kPar = 2 * 3 * BN * 4;             // {s_w, wsum, bias} x 2 tiles
   static constexpr int offA = 0;
+  // W4A8: the unpacked s8 B tiles live in their own kCB-deep ring, decoupled
+  // from the TMA ring (A + packed nibbles), so the TMA ring can be deep
+  static constexpr int kCB = kW4 ? 3 : kStages;
   static constexpr int offB = offA + kStages * kA;
-  static constexpr int offP = offB + kStages * kB;
+  static constexpr int offP = offB + kCB * kB;
   static constexpr int offE = offP + kStages * kP;
   static constexpr int offPar = offE + kEpi;
   static constexpr int offBar = offPar + kPar;
-  static constexpr int kBars = kStages * 3 + 4;
+  // full[kStages], empty[kStages], conv[kCB], bempty[kCB], tfull[2], tempty[2]
+  static constexpr int kBars = kStages * 2 + kCB * 2 + 4;
   static constexpr int bytes = offBar + kBars * 8 + 16;
   static constexpr int alloc = bytes + 1024;  // manual 1024-byte alignment
   static_assert(alloc <= 227 * 1024, "shared memory budget exceeded");
@@ -133,8 +137,9 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
   uint32_t* sPar = reinterpret_cast<uint32_t*>(smem + L::offPar);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::offBar);
   uint64_t* empty = full + kStages;
-  uint64_t* conv = empty + kStages;
-  uint64_t* tfull = conv + kStages;
+  uint64_t* conv = empty + kStages;   // [kCB] W4: unpacked B buffer ready
+  uint64_t* bempty = conv + L::kCB;   // [kCB] W4: unpacked B buffer consumed
+  uint64_t* tfull = bempty + L::kCB;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -169,7 +174,10 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&conv[s], kConvWarps * (k2Cta ? 2 : 1));  // leader's: both CTAs convert
+    }
+    for (int c = 0; c < L::kCB; ++c) {
+      mbar_init(&conv[c], kConvWarps * (k2Cta ? 2 : 1));  // leader's: both CTAs convert
+      mbar_init(&bempty[c], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -236,6 +244,8 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
+      int cb = 0;            // W4: unpacked-B ring slot
+      uint32_t cph = 0;
       for (int tile = tile0; tile < total_tiles; tile += tstride, ++it) {
         const int acc = it & 1;
         const uint32_t aph = (it >> 1) & 1;
@@ -244,10 +254,10 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         const uint32_t d = tmem_base + acc * BN;
         for (int kb = 0; kb < g.k_blocks; ++kb) {
           timed_wait(&full[s], ph, pw0);
-          if constexpr (kW4) mbar_wait(&conv[s], ph);
+          if constexpr (kW4) mbar_wait(&conv[cb], cph);
           tc_fence_after();
           const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * L::kA));
-          const uint64_t bd = umma_desc_sw128(smem_u32(sB + s * L::kB));
+          const uint64_t bd = umma_desc_sw128(smem_u32(sB + (kW4 ? cb : s) * L::kB));
 #pragma unroll
           for (int k = 0; k < BK / 32; ++k) {
             if constexpr (k2Cta)
@@ -259,6 +269,17 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
             mma_commit_cta2_mc(&empty[s], 0x3);
           else
             mma_commit(&empty[s]);
+          if constexpr (kW4) {
+            // the unpacked B buffer is free once these MMAs have read it
+            if constexpr (k2Cta)
+              mma_commit_cta2_mc(&bempty[cb], 0x3);
+            else
+              mma_commit(&bempty[cb]);
+            if (++cb == L::kCB) {
+              cb = 0;
+              cph ^= 1;
+            }
+          }
           if (++s == kStages) {
             s = 0;
             ph ^= 1;
@@ -497,11 +518,14 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     const int ct = threadIdx.x - 32 * kEpiWarps;  // 0..127
     int s = 0;
     uint32_t ph = 0;
+    int cb = 0;
+    uint32_t cph = 0;
     for (int tile = tile0; tile < total_tiles; tile += tstride) {
       for (int kb = 0; kb < g.k_blocks; ++kb) {
         mbar_wait(&full[s], ph);
+        mbar_wait(&bempty[cb], cph ^ 1);  // the MMA has finished with this B buffer
         const uint8_t* src = sP + s * L::kP;
-        uint8_t* dst = sB + s * L::kB;
+        uint8_t* dst = sB + cb * L::kB;
         // this CTA's B rows x 8 granules of 16 output bytes (= 8 packed bytes each)
 #pragma unroll 4
         for (int item = ct; item < L::kBRows * 8; item += 32 * kConvWarps) {
@@ -515,9 +539,13 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         __syncwarp();
         if (lane == 0) {
           if constexpr (k2Cta)  // the leader's MMA reads both CTAs' B halves
-            mbar_arrive_cluster_release(mapa_shared(smem_u32(&conv[s]), 0));
+            mbar_arrive_cluster_release(mapa_shared(smem_u32(&conv[cb]), 0));
           else
-            mbar_arrive(&conv[s]);
+            mbar_arrive(&conv[cb]);
+        }
+        if (++cb == L::kCB) {
+          cb = 0;
+          cph ^= 1;
         }
         if (++s == kStages) {
           s = 0;

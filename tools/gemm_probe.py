@@ -1,6 +1,6 @@
 """Per-role wait cycles of the GEMM (DTQ_DEBUG_GEMM_PROBE=1 diagnostics).
 
-usage: DTQ_DEBUG_GEMM_PROBE=1 python tools/gemm_probe.py M N K
+usage: DTQ_DEBUG_GEMM_PROBE=1 python tools/gemm_probe.py M N K [wbits]
 """
 import ctypes as C
 import os
@@ -13,10 +13,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2406_02540_b200 as dtq  # noqa: E402
 
 M, N, K = (int(v) for v in sys.argv[1:4])
+WB = int(sys.argv[4]) if len(sys.argv) > 4 else 8
 dev = torch.device("cuda:0")
 x = torch.randn(M, K, device=dev).half()
 w = (torch.randn(N, K, device=dev) / K ** 0.5).half()
-layer = dtq.QuantLinear.create(w, 8, 8)
+layer = dtq.QuantLinear.create(w, WB, 8)
 codes, s, z = layer.quantize(x)
 y = torch.empty(M, N, dtype=torch.float16, device=dev)
 for _ in range(3):

@@ -40,6 +40,8 @@
 // smem = fq_tile_layout(...).bytes.
 #pragma once
 
+#include <cstdlib>
+
 #include "fused_quant.cuh"
 #include "ptx.cuh"
 
@@ -55,7 +57,21 @@ struct FqShape {
   static constexpr int kRuns = kE / 16;    // 16-column runs
   static constexpr int kItems = 32 / kQ;   // (row, block) items per warp
 };
-__host__ __device__ constexpr int fq_lanes(int64_t K) { return K <= 2304 ? 4 : 2; }
+// DTQ_FQ_WIDE_K (diagnostics) moves the two-lane threshold; default 2304
+__host__ inline int64_t fq_wide_k() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("DTQ_FQ_WIDE_K");
+    return e ? static_cast<int64_t>(std::atoll(e)) : int64_t{2304};
+  }();
+  return v;
+}
+__host__ __device__ inline int fq_lanes(int64_t K) {
+#ifdef __CUDA_ARCH__
+  return K <= 2304 ? 4 : 2;
+#else
+  return K <= fq_wide_k() ? 4 : 2;
+#endif
+}
 
 struct TileLayout {
   size_t pitch_in;

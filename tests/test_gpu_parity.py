@@ -71,7 +71,7 @@ def test_quantizer_full_size_bitexact(oracle, dtype):
     assert np.array_equal(z.cpu().numpy(), z_ref)
 
 
-@pytest.mark.parametrize("K", [8, 40, 136, 200, 1000, 4608, 9216])
+@pytest.mark.parametrize("K", [8, 40, 128, 136, 200, 1000, 1152, 2304, 2432, 4608, 8192, 9216])
 def test_quantizer_ragged_and_wide(oracle, K):
     rng = np.random.default_rng(K)
     x = (rng.standard_normal((37, K)) * 3).astype(np.float16)
@@ -124,9 +124,11 @@ def test_balance_exact_mode_bitexact(golden):
     assert np.array_equal(s.cpu().numpy(), golden["rot_s"])
 
 
-def test_balance_fast_mode_within_one_lsb(oracle):
-    rng = np.random.default_rng(21)
-    M, K = 4096, 1152
+@pytest.mark.parametrize("M,K", [(4096, 1152), (1000, 4608), (37, 2304), (5, 128), (300, 2432)])
+def test_balance_fast_mode_within_one_lsb(oracle, M, K):
+    # the tile quantizer: 4 lanes per block up to K = 2304, 2 beyond; ragged
+    # row tiles (M not a multiple of the tile height)
+    rng = np.random.default_rng(21 + K)
     x = activations(rng, M, K)
     w = rng.standard_normal((256, K)) / np.sqrt(K)
     smooth = oracle.scaling_mask(np.abs(f64(x)).max(0), np.abs(w).max(0), 0.5)
@@ -254,18 +256,19 @@ def test_prologue_modulate_exact(oracle):
     assert d.max() <= 1 and (d > 0).mean() <= 1e-3
 
 
-def test_prologue_gelu_and_layernorm_run():
+@pytest.mark.parametrize("K", [1152, 4608])
+def test_prologue_gelu_and_layernorm_run(K):
     # GELU follows toydit.cpp:83; LayerNorm has no reference oracle (unpinned):
     # compare with a torch fp64 restatement by tolerance only
     rng = np.random.default_rng(9)
-    x = activations(rng, 128, 1152).astype(np.float32)
+    x = activations(rng, 128, K).astype(np.float32)
     xt = cuda(x)
     xd = torch.from_numpy(x).double()
     g = 0.5 * xd * (1 + torch.erf(xd / 2 ** 0.5))
     codes, s, z = dtq.quantize_rows(xt, prologue=dtq.Prologue(dtq.PROLOGUE_GELU))
     deq = (codes.double().cpu() - z.cpu()[:, None].double()) * s.cpu()[:, None]
     assert (deq - g).abs().max() <= s.cpu().max() * 0.51 + 1e-4
-    sc = torch.zeros(1152, device=DEV)
+    sc = torch.zeros(K, device=DEV)
     pro = dtq.Prologue(dtq.PROLOGUE_LN_MODULATE, sc, sc, 1e-6)
     codes, s, z = dtq.quantize_rows(xt, prologue=pro)
     ln = (xd - xd.mean(1, keepdim=True)) / torch.sqrt(xd.var(1, unbiased=False, keepdim=True) + 1e-6)

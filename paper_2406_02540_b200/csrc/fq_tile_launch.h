@@ -24,10 +24,27 @@ cudaError_t launch_tile(const dtq_fq::FqArgs& a, int R, int sms, cudaStream_t st
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, L.bytes);
   if (e != cudaSuccess) return e;
   const int64_t tiles = (a.M + R - 1) / R;
+  static const int occ_cap = [] {  // DTQ_FQ_OCC (diagnostics): CTAs per SM cap
+    const char* e = std::getenv("DTQ_FQ_OCC");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (occ_cap > 0 && occ > occ_cap) occ = occ_cap;
   const int64_t cap = static_cast<int64_t>(sms) * (occ > 0 ? occ : 1);
   const int grid = static_cast<int>(tiles < cap ? tiles : cap);
-  kern<<<grid, block, L.bytes, st>>>(a, R);
-  return cudaGetLastError();
+  // programmatic dependent launch: the CTAs' setup (barriers, the per-column
+  // table) overlaps the tail of the kernel that produces X; the kernel waits
+  // (griddepcontrol.wait) before its first read of X or of per-call inputs
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = L.bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, R);
 }
 
 template <typename Tin, int kPro>

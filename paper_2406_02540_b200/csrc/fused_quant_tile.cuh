@@ -266,20 +266,41 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
           : "memory");
   };
   int64_t tile = blockIdx.x;
+#ifdef FQ_TILE_PROBE
+  const unsigned long long pr_g0 = dtq_ptx::globaltimer_ns();
+#endif
   dtq_ptx::pdl_launch_dependents();  // let the GEMM that consumes the codes launch early
-  // warp 0: barriers, then the first tile's copies (overlap the table setup)
-  if (warp == 0) {
-    if (lane == 0) {
-      dtq_ptx::mbar_init(bar, 1);
-      dtq_ptx::mbar_init(bar + 1, 1);
-      dtq_ptx::fence_barrier_init();
+  // warp 0: barriers, then the first tile's copies (overlap the table setup).
+  // Under programmatic dependent launch everything before pdl_wait() runs
+  // while the kernel producing X drains: only layer constants are read there.
+  if (warp == 0 && lane == 0) {
+    dtq_ptx::mbar_init(bar, 1);
+    dtq_ptx::mbar_init(bar + 1, 1);
+    dtq_ptx::fence_barrier_init();
+  }
+  if (!has_b && a.col_mul != nullptr) {  // the folded table of a balanced layer: constants
+    for (int c0 = t; c0 < K; c0 += 8 * blockDim.x) {
+      float m[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * blockDim.x;
+        m[u] = c < K ? __ldg(a.col_mul + c) : 1.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * blockDim.x;
+        if (c < K) colA[c] = m[u];
+      }
     }
+  }
+  dtq_ptx::pdl_wait();  // X (and the modulate vectors) come from earlier kernels
+  if (warp == 0) {
     __syncwarp();
     if (tile < ntiles) issue(tile, 0);
   }
-  // folded per-column affine map: v -> v * A_c + B_c.  Loads are batched
-  // 8 deep per thread so the table costs one L2 round trip, not eight.
-  if (has_a) {
+  // folded per-column affine map with the per-call modulate vectors:
+  // v -> v * A_c + B_c.  Loads are batched 8 deep per thread.
+  if constexpr (has_b) {
     for (int c0 = t; c0 < K; c0 += 8 * blockDim.x) {
       float m[8], sc[8], sh[8];
 #pragma unroll
@@ -559,12 +580,16 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
     else
       fq_tile_codes<kFqQ, false, kExactV>(P, inv_sf, zm, qmax_i, s, z, qmax, dst);
   }
+#ifdef FQ_TILE_PROBE
   if (probe) {
-    unsigned long long* pr = a.probe + blockIdx.x * 4;
+    unsigned long long* pr = a.probe + blockIdx.x * 8;
     pr[0] = static_cast<unsigned long long>(pr_wait);
     pr[1] = static_cast<unsigned long long>(pr_bar);
     pr[2] = static_cast<unsigned long long>(clock64() - pr_t0);
+    pr[3] = pr_g0;                        // CTA start (globaltimer ns)
+    pr[4] = dtq_ptx::globaltimer_ns();    // CTA end
   }
+#endif
 }
 
 #undef FQ_V

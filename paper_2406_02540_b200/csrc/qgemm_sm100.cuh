@@ -199,6 +199,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();  // A codes, s_x, z_x come from the preceding quantizer kernel
+  pdl_launch_dependents();  // the next layer's quantizer may set up on freed SMs
 
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer

@@ -35,25 +35,28 @@ def one(M, K, pro, rot, dtype, reps=50):
     codes = torch.empty(M, (K + 15) // 16 * 16, dtype=torch.uint8, device=dev)[:, :K]
     s = torch.empty(M, dtype=torch.float64, device=dev)
     z = torch.empty(M, dtype=torch.int32, device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    # a ring of input copies larger than L2 (126 MB): every launch reads cold
+    # data; batches of launches between two events (the event clock ticks in
+    # ~2 us steps, too coarse for one small kernel)
+    nbuf = max(2, int(256e6 // x.numel() // x.element_size()) + 1)
+    xs = [x.clone() for _ in range(nbuf)]
+    batch = 20
 
-    def run():
-        layer.quantize(x, mode=dtq.MODE_FAST, out=(codes, s, z), prologue=prologue)
+    def run(i=0):
+        layer.quantize(xs[i % nbuf], mode=dtq.MODE_FAST, out=(codes, s, z), prologue=prologue)
 
-    for _ in range(3):
-        run()
+    for i in range(3):
+        run(i)
     torch.cuda.synchronize()
     ts = []
-    warm = os.environ.get("FQ_WARM") == "1"
-    for i in range(reps):
-        if not warm:
-            flush.fill_(i & 255)
+    for r in range(reps // 5 + 3):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        run()
+        for i in range(batch):
+            run(r * batch + i)
         b.record()
         b.synchronize()
-        ts.append(a.elapsed_time(b) * 1e3)
+        ts.append(a.elapsed_time(b) * 1e3 / batch)
     ts.sort()
     med = ts[len(ts) // 2]
     nbytes = M * K * (x.element_size() + 1) + 12 * M

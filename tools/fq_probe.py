@@ -31,7 +31,10 @@ layer.quantize(x)
 torch.cuda.synchronize()
 host = (C.c_uint64 * (65536 * 8))()
 cud.cudaMemcpy(host, C.c_void_p(ptr), 65536 * 8 * 8, 2)
-a = np.frombuffer(host, dtype=np.uint64).reshape(-1, 4)[:, :3].astype(np.float64)
+a = np.frombuffer(host, dtype=np.uint64).reshape(-1, 8)[:, :5].astype(np.float64)
 a = a[a[:, 2] > 0]
+t0 = a[:, 3].min()
 print(f"CTAs {len(a)}: data-wait {a[:, 0].mean():.0f}  barrier {a[:, 1].mean():.0f}  "
-      f"total {a[:, 2].mean():.0f} cycles (max total {a[:, 2].max():.0f})")
+      f"loop {a[:, 2].mean():.0f} cycles (max {a[:, 2].max():.0f}); CTA start spread "
+      f"{(a[:, 3].max() - t0) / 1e3:.2f} us, lifetime mean {(a[:, 4] - a[:, 3]).mean() / 1e3:.2f} us, "
+      f"last end {(a[:, 4].max() - t0) / 1e3:.2f} us after first start")

@@ -14,19 +14,22 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2406_02540_b200 as dtq  # noqa: E402
 
 
-def timeit(fn, flush, reps=30):
-    for _ in range(3):
-        fn()
+def timeit(fn, flush, reps=30, batch=10):
+    """Mean time per call over batches of `batch` back-to-back calls between
+    two events (the event clock ticks in ~2 us steps); fn(i) should rotate
+    through inputs larger than L2."""
+    for i in range(3):
+        fn(i)
     torch.cuda.synchronize()
     ts = []
-    for i in range(reps):
-        flush.fill_(i & 255)
+    for r in range(max(3, reps // 5)):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        fn()
+        for i in range(batch):
+            fn(r * batch + i)
         b.record()
         b.synchronize()
-        ts.append(a.elapsed_time(b) * 1e3)
+        ts.append(a.elapsed_time(b) * 1e3 / batch)
     ts.sort()
     return ts[len(ts) // 2]
 
@@ -39,12 +42,16 @@ def one(M, N, K, wbits):
     layer = dtq.QuantLinear.create(w, wbits, 8)
     codes, s, z = layer.quantize(x)
     y = torch.empty(M, N, dtype=torch.float16, device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    t = timeit(lambda: layer.gemm(codes, s, z, out=y), flush)
-    a8 = torch.randint(-127, 127, (M, K), dtype=torch.int8, device=dev)
+    flush = None
+    nb = max(2, int(256e6 // (M * K)) + 1)   # code buffers cycling through > L2
+    cs = [codes.clone() for _ in range(nb)]
+    t = timeit(lambda i: layer.gemm(cs[i % nb], s, z, out=y), flush)
+    a8s = [torch.randint(-127, 127, (M, K), dtype=torch.int8, device=dev) for _ in range(nb)]
     b8 = torch.randint(-127, 127, (K, N), dtype=torch.int8, device=dev).t().contiguous().t()
-    ti = timeit(lambda: torch._int_mm(a8, b8), flush)
-    th = timeit(lambda: torch.matmul(x, w.t(), out=y), flush)
+    ti = timeit(lambda i: torch._int_mm(a8s[i % nb], b8), flush)
+    nh = max(2, int(256e6 // (2 * M * K)) + 1)
+    xs = [x.clone() for _ in range(nh)]
+    th = timeit(lambda i: torch.matmul(xs[i % nh], w.t(), out=y), flush)
     ops = 2.0 * M * N * K
     print(f"M={M} N={N} K={K} W{wbits}: ours {t:.1f} us {ops / t / 1e6:.0f} TOPS | "
           f"cublasLt int8 {ti:.1f} us {ops / ti / 1e6:.0f} | fp16 {th:.1f} us {ops / th / 1e6:.0f}",

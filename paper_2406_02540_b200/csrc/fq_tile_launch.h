@@ -2,10 +2,43 @@
 // per-dtype translation units (fq_tile.cu, fq_tile_f16.cu, fq_tile_bf16.cu).
 #pragma once
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "fused_quant_tile.cuh"
 
 namespace {  // NOLINT
+
+// Launch attributes and occupancy per (kernel, device, block, smem): the
+// occupancy query costs microseconds of host time, more than a small launch
+// takes on the GPU, so it is made once.
+inline cudaError_t fq_tile_occupancy(const void* kern, int block, size_t smem, int* occ) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, size_t>, int> cache;
+  static std::map<std::pair<const void*, int>, size_t> smem_max;  // attribute only grows
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_tuple(kern, dev, block, smem);
+  std::lock_guard<std::mutex> lock(mu);
+  const auto it = cache.find(key);
+  if (it != cache.end()) {
+    *occ = it->second;
+    return cudaSuccess;
+  }
+  size_t& mx = smem_max[std::make_pair(kern, dev)];
+  if (smem > mx) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    mx = smem;
+  }
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, block, smem);
+  if (e != cudaSuccess) return e;
+  cache[key] = *occ;
+  return cudaSuccess;
+}
 
 template <typename Tin, bool kRot, bool kExactV, int kPro>
 cudaError_t launch_tile(const dtq_fq::FqArgs& a, int R, int sms, cudaStream_t st) {
@@ -17,11 +50,8 @@ cudaError_t launch_tile(const dtq_fq::FqArgs& a, int R, int sms, cudaStream_t st
   const dtq_fq::TileLayout L = dtq_fq::fq_tile_layout(a.K, R, sizeof(Tin), has_a, has_b);
   const int nb = static_cast<int>(a.K / 128);
   const int block = dtq_fq::fq_tile_threads(a.K, R);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(L.bytes));
-  if (e != cudaSuccess) return e;
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, L.bytes);
+  cudaError_t e = fq_tile_occupancy(reinterpret_cast<const void*>(kern), block, L.bytes, &occ);
   if (e != cudaSuccess) return e;
   const int64_t tiles = (a.M + R - 1) / R;
   static const int occ_cap = [] {  // DTQ_FQ_OCC (diagnostics): CTAs per SM cap

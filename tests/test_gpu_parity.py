@@ -345,3 +345,16 @@ def test_forward_host_pipelined_chunks_match_device_forward():
     yh = torch.empty((M, N), dtype=torch.float16).pin_memory()
     layer.forward_host(xh, yh)
     assert torch.equal(yh, want)
+
+
+@pytest.mark.gpu
+def test_tile_quantizer_varying_tile_heights_in_one_process():
+    # the tile height R (and so the kernel's dynamic smem) changes with M:
+    # a small-M launch must not shrink the smem limit a later launch needs
+    K = 1152
+    signs = torch.from_numpy(dtq.hadamard_signs(K, 7)).to(DEV)
+    bal = dtq.Balance(torch.ones(K, dtype=torch.float64, device=DEV) * 1.5, signs, 128)
+    for M in (16384, 480, 16384, 37, 4096, 5):
+        x = torch.randn(M, K, device=DEV).half()
+        codes, s, z = dtq.quantize_rows(x, balance=bal)
+        assert codes.shape == (M, K) and bool(torch.isfinite(s).all())

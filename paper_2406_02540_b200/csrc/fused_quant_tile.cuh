@@ -30,8 +30,9 @@
 //   * kExactV (no prologue, smoothing or rotation: v is the exact input, so
 //     the reference codes are reachable bit for bit): the exact residual
 //     e = fma(v, 1/s, (z + 1.5*2^23) - r) is checked, and |e| > 1/2 - 2^-15
-//     (|v/s - v*fl(1/s)| <= 2^-16 < the margin) re-evaluates that group of
-//     16 values with IEEE fp64 divides (rare, out of line);
+//     (|v/s - v*fl(1/s)| <= 2^-16 < the margin) re-checks that run of 16
+//     values in registers and re-evaluates the flagged ones with an IEEE
+//     fp64 divide (out of line; fp16 data has ~1e-4 exact ties);
 //   * a lane pair's 2 x 16 codes per run are one contiguous 32-byte sector:
 //     16-byte stores straight from registers, no staging, no barrier.
 //
@@ -111,28 +112,10 @@ __device__ __forceinline__ float min3f(float a, float b, float c) {
 
 constexpr float kFqTie = 0.5f - 3.0517578125e-05f;  // 1/2 - 2^-15
 
-// Exact re-evaluation (quant.cpp:169-175 in fp64) of the flagged 16-value
-// runs of one lane: v[16m + i] is run m, w[4m .. 4m+3] its packed codes.
-static __device__ __noinline__ void fq_tile_fix(const float* v, uint32_t* w, int nruns,
-                                                unsigned runs, float inv_sf, float zm, double s,
-                                                double z, double qmax) {
-#pragma unroll 1
-  for (int m = 0; m < nruns; ++m) {
-    if (!((runs >> m) & 1u)) continue;
-#pragma unroll 1
-    for (int i = 0; i < 16; ++i) {
-      const float x = v[16 * m + i];
-      const float rr = fmaf(x, inv_sf, zm);
-      const float e = fmaf(x, inv_sf, zm - rr);
-      if (fabsf(e) > kFqTie) {
-        const uint32_t c =
-            static_cast<uint32_t>(fmin(fmax(rint(static_cast<double>(x) / s) + z, 0.0), qmax));
-        const int word = 4 * m + (i >> 2);
-        const uint32_t sh = 8u * (i & 3);
-        w[word] = (w[word] & ~(0xffu << sh)) | (c << sh);
-      }
-    }
-  }
+// One exact code (quant.cpp:169-175 in fp64), out of line: called only for a
+// value whose fp32 evaluation lies within 2^-15 of a rounding tie.
+static __device__ __noinline__ uint32_t fq_exact_code(float x, double s, double z, double qmax) {
+  return static_cast<uint32_t>(fmin(fmax(rint(static_cast<double>(x) / s) + z, 0.0), qmax));
 }
 
 // 16 raw elements at p (smem) -> fp32
@@ -160,8 +143,8 @@ __device__ __forceinline__ void ld16(const uint8_t* p, float (&o)[16]) {
 // kE codes of one lane -> one 16-byte store per run (run m at dst + 16*kQ*m)
 template <int kQ, bool kClamp, bool kExactV>
 __device__ __forceinline__ void fq_tile_codes(const float2 (&P)[FqShape<kQ>::kPairs], float inv_sf,
-                                              float zm,
-                                              int qmax_i, double s, double z, double qmax,
+                                              float zm, int qmax_i, double s_num, double s_den,
+                                              double z, double qmax,
                                               uint8_t* __restrict__ dst) {
   const float2 inv2 = make_float2(inv_sf, inv_sf), zm2 = make_float2(zm, zm);
   const float2 neg = make_float2(-1.f, -1.f);
@@ -205,11 +188,24 @@ __device__ __forceinline__ void fq_tile_codes(const float2 (&P)[FqShape<kQ>::kPa
 #pragma unroll
     for (int m = 0; m < S::kRuns; ++m) runs |= (em[m] > kFqTie ? 1u : 0u) << m;
     if (runs) {
-      // copy out (keeps P itself in registers) and re-evaluate exactly
-      float vb[S::kE];
+      // possible fp32 ties: re-check each value of a flagged run in
+      // registers; only a confirmed near-tie pays the out-of-line fp64 divide
+      const double s = s_num / s_den;
 #pragma unroll
-      for (int l = 0; l < S::kE; ++l) vb[l] = FQ_V(P, l);
-      fq_tile_fix(vb, w, S::kRuns, runs, inv_sf, zm, s, z, qmax);
+      for (int m = 0; m < S::kRuns; ++m) {
+        if (!((runs >> m) & 1u)) continue;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float x = FQ_V(P, 16 * m + i);
+          const float rr = fmaf(x, inv_sf, zm);
+          const float e = fmaf(x, inv_sf, zm - rr);
+          if (fabsf(e) > kFqTie) {
+            const uint32_t c = fq_exact_code(x, s, z, qmax);
+            const uint32_t sh = 8u * (i & 3);
+            w[4 * m + (i >> 2)] = (w[4 * m + (i >> 2)] & ~(0xffu << sh)) | (c << sh);
+          }
+        }
+      }
     }
   }
 #pragma unroll
@@ -552,33 +548,41 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
         zf = static_cast<float>(fmin(fmax(rint(-static_cast<double>(lo) / sd), 0.0), qmax));
       }
     }
-    double s = 0.0;
-    const bool writer = b == 0 && p == 0;
-    if (writer || kExactV) {
+    // s = num / den in fp64 (quant.cpp:90-124); only the writer lane forms
+    // it (and the rare exact re-evaluation); kExactV needs fl32(1/s) = one
+    // fp64 divide den / num per thread
+    double num, den;
+    {
       const double dmn = static_cast<double>(mn), dmx = static_cast<double>(mx);
       if (a.symmetric) {
         const double amax = fmax(fabs(dmn), fabs(dmx));
-        s = amax > 0.0 ? amax / static_cast<double>((1 << (a.bits - 1)) - 1) : 1.0;
+        num = amax > 0.0 ? amax : 1.0;
+        den = amax > 0.0 ? static_cast<double>((1 << (a.bits - 1)) - 1) : 1.0;
       } else if (dmx == dmn) {
-        s = 1.0;
+        num = 1.0;
+        den = 1.0;
       } else {
-        s = (fmax(dmx, 0.0) - fmin(dmn, 0.0)) / qmax;
-      }
-      if (kExactV) inv_sf = static_cast<float>(1.0 / s);
-      if (writer) {
-        a.scale[row] = s;
-        a.zero[row] = static_cast<int32_t>(zf);
+        num = fmax(dmx, 0.0) - fmin(dmn, 0.0);
+        den = qmax;
       }
     }
+    const bool writer = b == 0 && p == 0;
+    double s = 0.0;
+    if (writer) {
+      s = num / den;
+      a.scale[row] = s;
+      a.zero[row] = static_cast<int32_t>(zf);
+    }
+    if constexpr (kExactV) inv_sf = static_cast<float>(den / num);
     const double z = static_cast<double>(zf);
     const float zm = zf + 12582912.0f;
 
     // ---- 5. codes straight from registers
     uint8_t* dst = a.codes + row * a.ldc + c0;
     if (clamp)
-      fq_tile_codes<kFqQ, true, kExactV>(P, inv_sf, zm, qmax_i, s, z, qmax, dst);
+      fq_tile_codes<kFqQ, true, kExactV>(P, inv_sf, zm, qmax_i, num, den, z, qmax, dst);
     else
-      fq_tile_codes<kFqQ, false, kExactV>(P, inv_sf, zm, qmax_i, s, z, qmax, dst);
+      fq_tile_codes<kFqQ, false, kExactV>(P, inv_sf, zm, qmax_i, num, den, z, qmax, dst);
   }
 #ifdef FQ_TILE_PROBE
   if (probe) {

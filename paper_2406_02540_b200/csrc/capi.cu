@@ -273,8 +273,9 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
     const bool has_b = kind == DTQ_PROLOGUE_MODULATE || kind == DTQ_PROLOGUE_LN_MODULATE;
     const bool has_a = has_b || col_mul != nullptr;
     const int R = dtq_fq_tile_rows(rows, cols, static_cast<int>(es), has_a, has_b, sms);
-    return fq_error(dtq_launch_fq_tile(a, static_cast<int>(es), x_dtype == DTQ_BF16 ? 1 : 0,
-                                       signs != nullptr, R, sms, st));
+    if (R > 0)
+      return fq_error(dtq_launch_fq_tile(a, static_cast<int>(es), x_dtype == DTQ_BF16 ? 1 : 0,
+                                         signs != nullptr, R, sms, st));
   }
   // fast: G 8-lane groups per row, R = 4/G rows per warp with R*K <= 4608
   // (18 KB fp32 park buffer per warp); warps per CTA sized for ~2 CTAs/SM

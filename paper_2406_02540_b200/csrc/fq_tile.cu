@@ -7,36 +7,31 @@
 
 #include "fq_tile_launch.h"
 
-// Rows per tile: the largest power of two <= 16 with <= 576 threads and the
-// CTA in 200 KB of smem (R = 16 at K = 1152: 288 threads, two CTAs per SM;
-// R = 8 at K = 4608: 576 threads, one), halved (down to 4) while the grid
-// would leave CTA slots idle.  DTQ_FQ_R overrides (diagnostics).
+// Rows per tile (compile-time in the kernel): 8, or 4 when an 8-row double
+// buffer of a wide row does not fit shared memory.  0 = the shape does not
+// fit the tile kernel at all (the caller uses the lane-group kernel).
 int dtq_fq_tile_rows(int64_t M, int64_t K, int es, bool has_a, bool has_b, int sms) {
-  // K <= 2304: four lanes per block, <= 288 threads (R = 8 at K = 1152);
-  // wider: two lanes per block, <= 576 threads (R = 8 at K = 4608)
-  const int cap = dtq_fq::fq_lanes(K) == 4 ? 288 : 576;
-  int R = 16;
-  while (R > 1 && (dtq_fq::fq_tile_threads(K, R) > cap ||
-                   dtq_fq::fq_tile_layout(K, R, es, has_a, has_b).bytes > 100 * 1024))
-    R >>= 1;
-  while (R > 4 && (M + R - 1) / R < 2 * sms) R >>= 1;
-  static const int forced = [] {
-    const char* e = std::getenv("DTQ_FQ_R");
-    return e ? std::atoi(e) : 0;
-  }();
-  if ((forced == 1 || forced == 2 || forced == 4 || forced == 8 || forced == 16) && dtq_fq::fq_tile_threads(K, forced) <= cap)
-    R = forced;
-  return R;
+  (void)M;
+  (void)sms;
+  constexpr size_t kMax = 220 * 1024;
+  const int cap = dtq_fq::fq_lanes(K) == 4 ? 288 : 576;  // the kernels' launch bounds
+  for (int R = 8; R >= 4; R -= 4)
+    if (dtq_fq::fq_tile_threads(K, R) <= cap &&
+        dtq_fq::fq_tile_layout(K, R, es, has_a, has_b, 2).bytes <= kMax &&
+        (R == 8 || dtq_fq::fq_lanes(K) == 2))
+      return R;
+  return 0;
 }
 
-cudaError_t dtq_launch_fq_tile_f16(const dtq_fq::FqArgs& a, bool rot, int R, int sms,
+cudaError_t dtq_launch_fq_tile_f16(const dtq_fq::FqArgs& a, bool rot, int R, int nbuf, int sms,
                                    cudaStream_t st);
-cudaError_t dtq_launch_fq_tile_bf16(const dtq_fq::FqArgs& a, bool rot, int R, int sms,
+cudaError_t dtq_launch_fq_tile_bf16(const dtq_fq::FqArgs& a, bool rot, int R, int nbuf, int sms,
                                     cudaStream_t st);
 
 cudaError_t dtq_launch_fq_tile(const dtq_fq::FqArgs& a, int x_dtype_size, int x_is_bf16, bool rot,
                                int R, int sms, cudaStream_t st) {
-  if (x_dtype_size == 4) return launch_rot<float>(a, rot, R, sms, st);
-  if (x_is_bf16) return dtq_launch_fq_tile_bf16(a, rot, R, sms, st);
-  return dtq_launch_fq_tile_f16(a, rot, R, sms, st);
+  const int nbuf = 2;  // input double buffer (deeper rings measured no faster)
+  if (x_dtype_size == 4) return launch_rot<float>(a, rot, R, nbuf, sms, st);
+  if (x_is_bf16) return dtq_launch_fq_tile_bf16(a, rot, R, nbuf, sms, st);
+  return dtq_launch_fq_tile_f16(a, rot, R, nbuf, sms, st);
 }

@@ -41,13 +41,16 @@ inline cudaError_t fq_tile_occupancy(const void* kern, int block, size_t smem, i
 }
 
 template <typename Tin, bool kRot, bool kExactV, int kPro>
-cudaError_t launch_tile(const dtq_fq::FqArgs& a, int R, int sms, cudaStream_t st) {
-  const bool wide = dtq_fq::fq_lanes(a.K) == 2;  // K > 2304: two lanes per block, 576 threads
-  auto kern = wide ? dtq_fq::fq_tile_kernel<Tin, kRot, kExactV, kPro, true>
-                   : dtq_fq::fq_tile_kernel<Tin, kRot, kExactV, kPro, false>;
+cudaError_t launch_tile(const dtq_fq::FqArgs& a, int R, int nbuf, int sms, cudaStream_t st) {
+  // K <= 1152: 4 lanes per block, 8-row tiles (288 threads); K <= 4608: 2
+  // lanes, 8 rows (576 threads); wider: 2 lanes, 4 rows
+  const bool wide = dtq_fq::fq_lanes(a.K) == 2;
+  auto kern = !wide ? dtq_fq::fq_tile_kernel<Tin, kRot, kExactV, kPro, false, 8>
+              : (R == 8 ? dtq_fq::fq_tile_kernel<Tin, kRot, kExactV, kPro, true, 8>
+                        : dtq_fq::fq_tile_kernel<Tin, kRot, kExactV, kPro, true, 4>);
   const bool has_b = a.pro == dtq_fq::kProModulate || a.pro == dtq_fq::kProLnModulate;
   const bool has_a = has_b || a.col_mul != nullptr;
-  const dtq_fq::TileLayout L = dtq_fq::fq_tile_layout(a.K, R, sizeof(Tin), has_a, has_b);
+  const dtq_fq::TileLayout L = dtq_fq::fq_tile_layout(a.K, R, sizeof(Tin), has_a, has_b, nbuf);
   const int nb = static_cast<int>(a.K / 128);
   const int block = dtq_fq::fq_tile_threads(a.K, R);
   int occ = 0;
@@ -74,26 +77,26 @@ cudaError_t launch_tile(const dtq_fq::FqArgs& a, int R, int sms, cudaStream_t st
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a, R);
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 template <typename Tin, int kPro>
-cudaError_t launch_p(const dtq_fq::FqArgs& a, bool rot, int R, int sms, cudaStream_t st) {
-  if (rot) return launch_tile<Tin, true, false, kPro>(a, R, sms, st);
+cudaError_t launch_p(const dtq_fq::FqArgs& a, bool rot, int R, int nbuf, int sms, cudaStream_t st) {
+  if (rot) return launch_tile<Tin, true, false, kPro>(a, R, nbuf, sms, st);
   if constexpr (kPro == dtq_fq::kProNone) {
     // no prologue, smoothing or rotation: codes are reachable bit for bit
-    if (a.col_mul == nullptr) return launch_tile<Tin, false, true, kPro>(a, R, sms, st);
+    if (a.col_mul == nullptr) return launch_tile<Tin, false, true, kPro>(a, R, nbuf, sms, st);
   }
-  return launch_tile<Tin, false, false, kPro>(a, R, sms, st);
+  return launch_tile<Tin, false, false, kPro>(a, R, nbuf, sms, st);
 }
 
 template <typename Tin>
-cudaError_t launch_rot(const dtq_fq::FqArgs& a, bool rot, int R, int sms, cudaStream_t st) {
+cudaError_t launch_rot(const dtq_fq::FqArgs& a, bool rot, int R, int nbuf, int sms, cudaStream_t st) {
   switch (a.pro) {
-    case dtq_fq::kProModulate: return launch_p<Tin, dtq_fq::kProModulate>(a, rot, R, sms, st);
-    case dtq_fq::kProGelu: return launch_p<Tin, dtq_fq::kProGelu>(a, rot, R, sms, st);
-    case dtq_fq::kProLnModulate: return launch_p<Tin, dtq_fq::kProLnModulate>(a, rot, R, sms, st);
-    default: return launch_p<Tin, dtq_fq::kProNone>(a, rot, R, sms, st);
+    case dtq_fq::kProModulate: return launch_p<Tin, dtq_fq::kProModulate>(a, rot, R, nbuf, sms, st);
+    case dtq_fq::kProGelu: return launch_p<Tin, dtq_fq::kProGelu>(a, rot, R, nbuf, sms, st);
+    case dtq_fq::kProLnModulate: return launch_p<Tin, dtq_fq::kProLnModulate>(a, rot, R, nbuf, sms, st);
+    default: return launch_p<Tin, dtq_fq::kProNone>(a, rot, R, nbuf, sms, st);
   }
 }
 

@@ -48,7 +48,7 @@
 
 namespace dtq_fq {
 
-// Lanes per 128-column block: kQ = 4 for K <= 2304 (32 values per lane,
+// Lanes per 128-column block: kQ = 4 for K <= 1152 (32 values per lane,
 // <= 72 registers, three 288-thread CTAs per SM), kQ = 2 for wider rows (64
 // values per lane, 576-thread CTAs).  Derived per-lane shapes:
 template <int kQ>
@@ -58,21 +58,24 @@ struct FqShape {
   static constexpr int kRuns = kE / 16;    // 16-column runs
   static constexpr int kItems = 32 / kQ;   // (row, block) items per warp
 };
-// DTQ_FQ_WIDE_K (diagnostics) moves the two-lane threshold; default 2304
+// DTQ_FQ_WIDE_K (diagnostics) moves the two-lane threshold; default 1152
+// (four lanes x 8 rows x nb blocks must stay within 288 threads)
 __host__ inline int64_t fq_wide_k() {
   static const int64_t v = [] {
     const char* e = std::getenv("DTQ_FQ_WIDE_K");
-    return e ? static_cast<int64_t>(std::atoll(e)) : int64_t{2304};
+    return e ? static_cast<int64_t>(std::atoll(e)) : int64_t{1152};
   }();
   return v;
 }
 __host__ __device__ inline int fq_lanes(int64_t K) {
 #ifdef __CUDA_ARCH__
-  return K <= 2304 ? 4 : 2;
+  return K <= 1152 ? 4 : 2;
 #else
   return K <= fq_wide_k() ? 4 : 2;
 #endif
 }
+
+constexpr int kFqMaxBuf = 4;  // input ring depth limit
 
 struct TileLayout {
   size_t pitch_in;
@@ -80,18 +83,18 @@ struct TileLayout {
 };
 
 __host__ __device__ inline TileLayout fq_tile_layout(int64_t K, int R, int es, bool has_a,
-                                                     bool has_b) {
+                                                     bool has_b, int nbuf = 2) {
   TileLayout L;
   const size_t nb = static_cast<size_t>(K) / 128;
   L.pitch_in = static_cast<size_t>(K) * es + 16;
   L.off_in1 = static_cast<size_t>(R) * L.pitch_in;
-  L.off_a = 2 * L.off_in1;
+  L.off_a = static_cast<size_t>(nbuf) * L.off_in1;  // nbuf-deep input ring
   L.off_b = L.off_a + (has_a ? static_cast<size_t>(K) * 4 : 0);
   L.off_red = L.off_b + (has_b ? static_cast<size_t>(K) * 4 : 0);
   // min/max pairs (double-buffered) + two LayerNorm partial arrays, nb x R each
   L.off_bar = L.off_red + nb * R * (2 * 8 + 4 + 4);
   L.off_bar = (L.off_bar + 7) / 8 * 8;
-  L.bytes = L.off_bar + 16;
+  L.bytes = L.off_bar + 8 * kFqMaxBuf;
   return L;
 }
 
@@ -214,11 +217,14 @@ __device__ __forceinline__ void fq_tile_codes(const float2 (&P)[FqShape<kQ>::kPa
         make_uint4(w[4 * m], w[4 * m + 1], w[4 * m + 2], w[4 * m + 3]);
 }
 
-// kWide: 576-thread CTAs (K > 2304, one per SM); otherwise <= 288 threads
+// kWide: 576-thread CTAs (K > 1152, one per SM); otherwise <= 288 threads
 // with registers capped for three CTAs per SM
-template <typename Tin, bool kRot, bool kExactV, int kPro, bool kWide>
+template <typename Tin, bool kRot, bool kExactV, int kPro, bool kWide, int kR>
 __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
-    fq_tile_kernel(const FqArgs a, const int R) {
+    fq_tile_kernel(const FqArgs a) {
+  // compile-time tile height and ring depth: the index arithmetic folds
+  constexpr int R = kR;
+  constexpr int nbuf = 2;
   constexpr int kFqQ = kWide ? 2 : 4;
   using S = FqShape<kFqQ>;
   constexpr int kFqE = S::kE, kFqPairs = S::kPairs, kFqRuns = S::kRuns, kFqItems = S::kItems;
@@ -236,13 +242,13 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
   const bool active = b_raw < nb;  // blockDim is rounded up to whole warps
   const int b = active ? b_raw : 0;
   const bool has_a = has_b || a.col_mul != nullptr;
-  const TileLayout L = fq_tile_layout(K, R, es, has_a, has_b);
+  const TileLayout L = fq_tile_layout(K, R, es, has_a, has_b, nbuf);
   float* colA = reinterpret_cast<float*>(fq_smem + L.off_a);
   float* colB = reinterpret_cast<float*>(fq_smem + L.off_b);
   float2* red_mm = reinterpret_cast<float2*>(fq_smem + L.off_red);
   float* red_s1 = reinterpret_cast<float*>(fq_smem + L.off_red + static_cast<size_t>(nb) * R * 16);
   float* red_s2 = red_s1 + nb * R;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(fq_smem + L.off_bar);  // [2]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fq_smem + L.off_bar);  // [nbuf]
   const uint8_t* __restrict__ X = static_cast<const uint8_t*>(a.x);
   const uint32_t row_bytes = static_cast<uint32_t>(K) * es;
 
@@ -270,8 +276,7 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
   // Under programmatic dependent launch everything before pdl_wait() runs
   // while the kernel producing X drains: only layer constants are read there.
   if (warp == 0 && lane == 0) {
-    dtq_ptx::mbar_init(bar, 1);
-    dtq_ptx::mbar_init(bar + 1, 1);
+    for (int i = 0; i < nbuf; ++i) dtq_ptx::mbar_init(bar + i, 1);
     dtq_ptx::fence_barrier_init();
   }
   if (!has_b && a.col_mul != nullptr) {  // the folded table of a balanced layer: constants
@@ -290,9 +295,10 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
     }
   }
   dtq_ptx::pdl_wait();  // X (and the modulate vectors) come from earlier kernels
-  if (warp == 0) {
+  if (warp == 0) {  // the ring's first nbuf - 1 tiles
     __syncwarp();
-    if (tile < ntiles) issue(tile, 0);
+    for (int k = 0; k + 1 < nbuf; ++k)
+      if (tile + k * static_cast<int64_t>(gridDim.x) < ntiles) issue(tile + k * gridDim.x, k);
   }
   // folded per-column affine map with the per-call modulate vectors:
   // v -> v * A_c + B_c.  Loads are batched 8 deep per thread.
@@ -339,17 +345,21 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
 #endif
   long long pr_t0 = probe ? clock64() : 0, pr_wait = 0, pr_bar = 0;
   for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
-    const int buf = it & 1;
+    const int buf = it % nbuf;
     const int64_t row = tile * R + r;
     const bool ok = active && row < a.M;
-    // prefetch the next tile into the other buffer (free since the last barrier)
-    if (warp == 0 && tile + gridDim.x < ntiles) {
-      dtq_ptx::fence_proxy_async_smem();
-      issue(tile + gridDim.x, buf ^ 1);
+    // prefetch nbuf - 1 tiles ahead into the buffer consumed last iteration
+    // (every thread loaded it into registers before that iteration's barrier)
+    {
+      const int64_t ahead = tile + static_cast<int64_t>(nbuf - 1) * gridDim.x;
+      if (warp == 0 && ahead < ntiles) {
+        dtq_ptx::fence_proxy_async_smem();
+        issue(ahead, (it + nbuf - 1) % nbuf);
+      }
     }
     {
       const long long w0 = probe ? clock64() : 0;
-      dtq_ptx::mbar_wait(bar + buf, (it >> 1) & 1);
+      dtq_ptx::mbar_wait(bar + buf, (it / nbuf) & 1);
       if (probe) pr_wait += clock64() - w0;
     }
 
@@ -509,7 +519,7 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
         mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       }
-      if (p == 0 && active) red_mm[(buf * nb + b) * R + r] = make_float2(mn, mx);
+      if (p == 0 && active) red_mm[((it & 1) * nb + b) * R + r] = make_float2(mn, mx);
     }
     {
       const long long b0 = probe ? clock64() : 0;
@@ -519,7 +529,7 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
     if (!ok) continue;
     float mn = __int_as_float(0x7f800000), mx = -mn;
     for (int j = 0; j < nb; ++j) {
-      const float2 m = red_mm[(buf * nb + j) * R + r];
+      const float2 m = red_mm[((it & 1) * nb + j) * R + r];
       mn = fminf(mn, m.x);
       mx = fmaxf(mx, m.y);
     }

@@ -51,7 +51,6 @@ cudaError_t launch_tile(const dtq_fq::FqArgs& a, int R, int nbuf, int sms, cudaS
   const bool has_b = a.pro == dtq_fq::kProModulate || a.pro == dtq_fq::kProLnModulate;
   const bool has_a = has_b || a.col_mul != nullptr;
   const dtq_fq::TileLayout L = dtq_fq::fq_tile_layout(a.K, R, sizeof(Tin), has_a, has_b, nbuf);
-  const int nb = static_cast<int>(a.K / 128);
   const int block = dtq_fq::fq_tile_threads(a.K, R);
   int occ = 0;
   cudaError_t e = fq_tile_occupancy(reinterpret_cast<const void*>(kern), block, L.bytes, &occ);

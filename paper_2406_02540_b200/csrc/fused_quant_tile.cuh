@@ -247,7 +247,6 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
   float* colB = reinterpret_cast<float*>(fq_smem + L.off_b);
   float2* red_mm = reinterpret_cast<float2*>(fq_smem + L.off_red);
   float* red_s1 = reinterpret_cast<float*>(fq_smem + L.off_red + static_cast<size_t>(nb) * R * 16);
-  float* red_s2 = red_s1 + nb * R;
   uint64_t* bar = reinterpret_cast<uint64_t*>(fq_smem + L.off_bar);  // [nbuf]
   const uint8_t* __restrict__ X = static_cast<const uint8_t*>(a.x);
   const uint32_t row_bytes = static_cast<uint32_t>(K) * es;
@@ -343,7 +342,10 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
 #else
   constexpr bool probe = false;
 #endif
-  long long pr_t0 = probe ? clock64() : 0, pr_wait = 0, pr_bar = 0;
+#ifdef FQ_TILE_PROBE
+  long long pr_t0 = probe ? clock64() : 0;
+#endif
+  long long pr_wait = 0, pr_bar = 0;
   for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
     const int buf = it % nbuf;
     const int64_t row = tile * R + r;
@@ -383,32 +385,47 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
 #pragma unroll
       for (int k = 0; k < kFqPairs; ++k) P[k] = gelu2(P[k]);
     } else if constexpr (kPro == kProLnModulate) {
+      // LayerNorm statistics in ONE exchange: per-thread mean and M2 (two
+      // passes over registers), merged across the lanes of a block and then
+      // across the row's blocks with Chan et al.'s pairwise update (equal
+      // counts), so a single CTA barrier suffices
       float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int k = 0; k < kFqPairs; ++k) s2 = __fadd2_rn(s2, P[k]);
-      float s1 = s2.x + s2.y;
+      float lm = (s2.x + s2.y) * (1.f / kFqE);
+      float2 q2 = make_float2(0.f, 0.f);
+      {
+        const float2 nm = make_float2(-lm, -lm);
 #pragma unroll
-      for (int o = kFqItems; o < 32; o <<= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      if (p == 0 && active) red_s1[b * R + r] = s1;
-      __syncthreads();
-      float tot = 0.f;
-      for (int j = 0; j < nb; ++j) tot += red_s1[j * R + r];
-      const float mean = tot / static_cast<float>(K);
-      const float2 nm = make_float2(-mean, -mean);
-      float2 qq = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int k = 0; k < kFqPairs; ++k) {
-        const float2 d = __fadd2_rn(P[k], nm);
-        qq = __ffma2_rn(d, d, qq);
+        for (int k = 0; k < kFqPairs; ++k) {
+          const float2 d = __fadd2_rn(P[k], nm);
+          q2 = __ffma2_rn(d, d, q2);
+        }
       }
-      float q1 = qq.x + qq.y;
+      float lM2 = q2.x + q2.y;
+      float n = static_cast<float>(kFqE);
 #pragma unroll
-      for (int o = kFqItems; o < 32; o <<= 1) q1 += __shfl_xor_sync(0xffffffffu, q1, o);
-      if (p == 0 && active) red_s2[b * R + r] = q1;
+      for (int o = kFqItems; o < 32; o <<= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, lm, o);
+        const float oM2 = __shfl_xor_sync(0xffffffffu, lM2, o);
+        const float d = om - lm;
+        lm = fmaf(d, 0.5f, lm);
+        lM2 = lM2 + oM2 + d * d * (0.5f * n);
+        n *= 2.f;
+      }
+      float2* red_ln = reinterpret_cast<float2*>(red_s1);  // (mean, M2) per (block, row)
+      if (p == 0 && active) red_ln[b * R + r] = make_float2(lm, lM2);
       __syncthreads();
-      float tq = 0.f;
-      for (int j = 0; j < nb; ++j) tq += red_s2[j * R + r];
-      const float rstd = rsqrtf(tq / static_cast<float>(K) + a.eps);
+      float2 st = red_ln[r];
+      for (int j = 1; j < nb; ++j) {
+        const float2 o = red_ln[j * R + r];
+        const float d = o.x - st.x;
+        const float inv = __frcp_rn(static_cast<float>(j + 1));
+        st.x = fmaf(d, inv, st.x);
+        st.y = st.y + o.y + d * d * (128.f * static_cast<float>(j) * inv);
+      }
+      const float mean = st.x;
+      const float rstd = rsqrtf(st.y / static_cast<float>(K) + a.eps);
       const float2 r2 = make_float2(rstd, rstd), o2 = make_float2(-mean * rstd, -mean * rstd);
 #pragma unroll
       for (int k = 0; k < kFqPairs; ++k) P[k] = __ffma2_rn(P[k], r2, o2);

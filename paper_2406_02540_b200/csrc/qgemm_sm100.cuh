@@ -388,8 +388,11 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
 #pragma unroll
           for (int j4 = 0; j4 < kPieceCols; j4 += 4) {
             const int cc = c * 32 + piece * kPieceCols + j4;
-            const uint4 sw4 = *reinterpret_cast<const uint4*>(par + cc);
-            const uint4 ws4 = *reinterpret_cast<const uint4*>(par + BN + cc);
+            const bool nolds = g.dbg == 7;  // diagnostics: params from registers, no LDS
+            const uint4 sw4 = nolds ? make_uint4(0x3f800000u, 0x3f800000u, 0x3f800000u, 0x3f800000u)
+                                    : *reinterpret_cast<const uint4*>(par + cc);
+            const uint4 ws4 = nolds ? make_uint4(0u, 0u, 0u, 0u)
+                                    : *reinterpret_cast<const uint4*>(par + BN + cc);
             // (no bias: skip the load -- the epilogue shares smem bandwidth with
             // the MMA operand reads and the TMA ring)
             const uint4 b4 = has_bias ? *reinterpret_cast<const uint4*>(par + 2 * BN + cc)
@@ -434,7 +437,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
               for (int u = 0; u < 4; ++u) w[j4 + u] = static_cast<uint32_t>(a32[u] >> (kW4 ? 4 : 0));
             }
           }
-          if (g.dbg == 3) {  // diagnostics: keep the math alive, skip staging + stores
+          if (g.dbg == 3 || g.dbg == 7) {  // diagnostics: keep the math alive, skip staging + stores
             uint32_t x = 0;
 #pragma unroll
             for (int i = 0; i < 16; ++i) x ^= w[i];

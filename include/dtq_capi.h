@@ -219,6 +219,36 @@ int dtq_balance_apply(const double* x, int64_t rows, int64_t cols, int64_t ldx,
 int dtq_matmul_nt_f64(const double* x, int64_t M, int64_t K, const double* w, int64_t N,
                       const double* bias, double* y, void* stream);
 
+/* ---------------------------------------------------------------- checkpoints
+ * read_checkpoint (trace_io.cpp:263-316) straight onto the device.  The
+ * file is the reference's little-endian format: "DTQCKPT\0", u16 version 1,
+ * u32 layer count, then per layer the name, shape, bits, grouping, symmetric
+ * flag, f32 scales (+ i32 zero points when asymmetric), the codes packed
+ * LSB-first (trace_io.cpp:79-91), the f32 scaling mask and the rotation
+ * signs as bits.  Bad magic / version / truncation / trailing bytes fail
+ * with DTQ_ERR_INVALID_ARGUMENT (the reference's FormatError). */
+typedef struct dtq_checkpoint_s* dtq_checkpoint_t;
+
+int dtq_checkpoint_open(const char* path, dtq_checkpoint_t* out);
+int dtq_checkpoint_close(dtq_checkpoint_t ck);
+int dtq_checkpoint_num_layers(dtq_checkpoint_t ck, int64_t* n);
+
+/* Layer i: name (NUL-terminated, owned by ck), C_out, C_in, weight bits,
+ * symmetric flag, mask length and rotation length (0 = none). */
+int dtq_checkpoint_layer_info(dtq_checkpoint_t ck, int64_t i, const char** name, int64_t* N,
+                              int64_t* K, int* bits, int* symmetric, int64_t* mask_len,
+                              int64_t* rot_len);
+
+/* Device-resident quantized linear of layer i.  The packed codes are
+ * uploaded as stored and unpacked on the device (W4: straight into the
+ * GEMM's nibble layout); the f32 scales become the fp64 s_w exactly as
+ * read_checkpoint widens them; the mask becomes the smoothing vector and the
+ * rotation signs the rotation, in blocks of `hblock` columns (0 = the
+ * stored rotation length).  Needs symmetric per-output-channel weights (the
+ * GEMM's layout): anything else is DTQ_ERR_UNSUPPORTED. */
+int dtq_checkpoint_load_layer(dtq_checkpoint_t ck, int64_t i, int act_bits, int hblock,
+                              void* stream, dtq_qlinear_t* out);
+
 #ifdef __cplusplus
 }
 #endif

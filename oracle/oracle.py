@@ -261,9 +261,54 @@ class Reference:
         L.dtq_ref_apply_scaling.argtypes = [_p, _i64, _p, _i64, _i64, _p]
         L.dtq_ref_pack_codes.restype = _i64
         L.dtq_ref_pack_codes.argtypes = [_p, _i64, _int, _p]
+        L.dtq_ref_write_checkpoint.argtypes = [C.c_char_p, _int, _p, _p, _p, _p, _p, _p, _p]
+        L.dtq_ref_read_checkpoint_layer.argtypes = [C.c_char_p, _i64, _p, _p, _p, _p]
 
     def round_even(self, v: float) -> float:
         return self.lib.dtq_ref_round_even(float(v))
+
+    def write_checkpoint(self, path: str, layers):
+        """layers: list of (name, W [N,K] f64, bits, mask [K] f32 or None,
+        rot [K] +-1 int8 or None) -> the reference's write_checkpoint."""
+        n = len(layers)
+        keep = []
+        names = (C.c_char_p * n)(*[l[0].encode() for l in layers])
+        ws = (C.c_void_p * n)()
+        Ns = np.zeros(n, np.int64)
+        Ks = np.zeros(n, np.int64)
+        bits = np.zeros(n, np.int32)
+        masks = (C.c_void_p * n)()
+        rots = (C.c_void_p * n)()
+        for i, (_, w, b, mask, rot) in enumerate(layers):
+            w = _f64(w)
+            keep.append(w)
+            ws[i] = w.ctypes.data
+            Ns[i], Ks[i] = w.shape
+            bits[i] = b
+            if mask is not None:
+                m = np.ascontiguousarray(mask, np.float32)
+                keep.append(m)
+                masks[i] = m.ctypes.data
+            if rot is not None:
+                r = np.ascontiguousarray(rot, np.int8)
+                keep.append(r)
+                rots[i] = r.ctypes.data
+        st = self.lib.dtq_ref_write_checkpoint(path.encode(), n, names, ws, Ns.ctypes.data,
+                                               Ks.ctypes.data, bits.ctypes.data, masks, rots)
+        if st:
+            raise RuntimeError(f"reference write_checkpoint failed ({st})")
+
+    def read_checkpoint_layer(self, path: str, i: int, N: int, K: int):
+        codes = np.zeros((N, K), np.uint8)
+        scale = np.zeros(N, np.float64)
+        zero = np.zeros(N, np.int32)
+        n = C.c_int64(0)
+        st = self.lib.dtq_ref_read_checkpoint_layer(path.encode(), i, codes.ctypes.data,
+                                                    scale.ctypes.data, zero.ctypes.data,
+                                                    C.byref(n))
+        if st:
+            raise RuntimeError(f"reference read_checkpoint failed ({st})")
+        return codes, scale, zero
 
     def quantize_rows(self, x, bits: int = 8, symmetric: bool = False):
         x = _f64(x)

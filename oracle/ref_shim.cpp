@@ -214,4 +214,44 @@ int64_t dtq_ref_pack_codes(const uint8_t* codes, int64_t count, int bits, uint8_
   return st ? -1 : n;
 }
 
+// trace_io.cpp:225-261: write a checkpoint of n layers, each quantized by the
+// reference's make_quant_linear path (quantize, per-output-channel,
+// symmetric) at bits[i]; mask[i] (length K[i] or 0) and rot[i] (+-1, length
+// K[i] or 0) are stored as given.  Used to generate tests/golden fixtures.
+int dtq_ref_write_checkpoint(const char* path, int n, const char* const* names,
+                             const double* const* w, const int64_t* N, const int64_t* K,
+                             const int* bits, const float* const* mask,
+                             const int8_t* const* rot) {
+  return guarded([&] {
+    dtq::QuantCheckpoint ck;
+    for (int i = 0; i < n; ++i) {
+      dtq::CheckpointLayer layer;
+      layer.name = names[i];
+      layer.weights = dtq::quantize(to_matrix(w[i], N[i], K[i]),
+                                    dtq::GroupingScheme::per_output_channel(), bits[i],
+                                    dtq::QuantMode::Dynamic, nullptr, /*symmetric=*/true);
+      if (mask[i]) layer.mask.assign(mask[i], mask[i] + K[i]);
+      if (rot[i]) layer.rotation_diag.assign(rot[i], rot[i] + K[i]);
+      ck.layers.push_back(std::move(layer));
+    }
+    dtq::write_checkpoint(path, ck);
+  });
+}
+
+// trace_io.cpp:263-316: read layer i back -- unpacked codes [N*K], the
+// per-row scales as read (f32 widened to f64) and the zero points.
+int dtq_ref_read_checkpoint_layer(const char* path, int64_t i, uint8_t* codes, double* scale,
+                                  int32_t* zero, int64_t* n_layers) {
+  return guarded([&] {
+    const dtq::QuantCheckpoint ck = dtq::read_checkpoint(path);
+    *n_layers = static_cast<int64_t>(ck.layers.size());
+    const auto& w = ck.layers.at(static_cast<std::size_t>(i)).weights;
+    std::memcpy(codes, w.ints.data(), w.ints.size());
+    for (std::size_t o = 0; o < w.params.size(); ++o) {
+      scale[o] = w.params[o].scale;
+      zero[o] = w.params[o].zero_point;
+    }
+  });
+}
+
 }  // extern "C"

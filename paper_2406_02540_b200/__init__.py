@@ -40,6 +40,8 @@ EXPORTED = (
     "dtq_qlinear_info", "dtq_qlinear_export", "dtq_qgemm", "dtq_qlinear_workspace_bytes",
     "dtq_qlinear_forward", "dtq_qlinear_quantize", "dtq_qlinear_forward_host",
     "dtq_quantize_static", "dtq_dequantize", "dtq_balance_apply", "dtq_matmul_nt_f64",
+    "dtq_checkpoint_open", "dtq_checkpoint_close", "dtq_checkpoint_num_layers",
+    "dtq_checkpoint_layer_info", "dtq_checkpoint_load_layer",
 )
 
 
@@ -82,6 +84,11 @@ def lib():
     L.dtq_qlinear_forward.argtypes = [p, i32, i64, i64, p, i32, p, p, i32, i64, p, C.c_size_t, p, p]
     L.dtq_qlinear_quantize.argtypes = [p, i32, i64, i64, p, i32, p, p, i64, p, p, p, p]
     L.dtq_qlinear_forward_host.argtypes = [p, i32, i64, p, i32, p, i32, p]
+    L.dtq_checkpoint_open.argtypes = [C.c_char_p, p]
+    L.dtq_checkpoint_close.argtypes = [p]
+    L.dtq_checkpoint_num_layers.argtypes = [p, p]
+    L.dtq_checkpoint_layer_info.argtypes = [p, i64, p, p, p, p, p, p, p]
+    L.dtq_checkpoint_load_layer.argtypes = [p, i64, i32, i32, p, p]
     _lib = L
     return L
 
@@ -293,6 +300,50 @@ class QuantLinear:
                                               self._h, mode, y_host.data_ptr(),
                                               _dtype_code(y_host.dtype), _stream(stream)))
         return y_host
+
+
+class Checkpoint:
+    """A reference quantized checkpoint (trace_io.cpp:225-316) loaded onto the
+    B200: `len(ck)` layers, `ck.info(i)`, `ck.load(i)` -> QuantLinear whose
+    packed codes were uploaded as stored and unpacked on the device."""
+
+    def __init__(self, path: str):
+        h = C.c_void_p()
+        _check(lib().dtq_checkpoint_open(os.fsencode(path), C.byref(h)))
+        self._h = h
+
+    def __len__(self) -> int:
+        n = C.c_int64(0)
+        _check(lib().dtq_checkpoint_num_layers(self._h, C.byref(n)))
+        return n.value
+
+    def info(self, i: int) -> dict:
+        name = C.c_char_p()
+        N, K, mlen, rlen = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        bits, sym = C.c_int(), C.c_int()
+        _check(lib().dtq_checkpoint_layer_info(self._h, i, C.byref(name), C.byref(N), C.byref(K),
+                                               C.byref(bits), C.byref(sym), C.byref(mlen),
+                                               C.byref(rlen)))
+        return {"name": name.value.decode(), "N": N.value, "K": K.value, "bits": bits.value,
+                "symmetric": bool(sym.value), "mask_len": mlen.value, "rot_len": rlen.value}
+
+    def load(self, i: int, act_bits: int = 8, hblock: int = 0, stream=None) -> "QuantLinear":
+        inf = self.info(i)
+        h = C.c_void_p()
+        _check(lib().dtq_checkpoint_load_layer(self._h, i, act_bits, hblock, _stream(stream),
+                                               C.byref(h)))
+        return QuantLinear(h.value, inf["N"], inf["K"], inf["bits"], act_bits, None)
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib().dtq_checkpoint_close(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def hadamard_signs(n: int, seed: int, randomize: bool = True):

@@ -14,8 +14,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/dtq_capi.h"
 #include "launch.h"
@@ -718,6 +720,120 @@ int forward_impl(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear
 
 }  // namespace
 
+namespace {
+
+// ------------------------------------------------------------------ checkpoints
+// Parser of the reference's quantized-checkpoint format (trace_io.cpp:
+// 225-316), restated: little-endian fields read with bounds checks, every
+// malformed input a DTQ_ERR_INVALID_ARGUMENT (the reference's FormatError).
+struct CkptLayer {
+  std::string name;
+  int64_t N = 0, K = 0;
+  int bits = 8;
+  int grouping = 0;
+  int64_t group_size = 0;
+  bool symmetric = true;
+  std::vector<float> scale;
+  std::vector<int32_t> zero;
+  std::vector<uint8_t> packed;  // LSB-first codes of all N*K weights
+  std::vector<float> mask;
+  std::vector<int8_t> rot;
+};
+
+struct CkptReader {
+  const std::vector<char>& buf;
+  size_t pos = 0;
+  bool ok = true;
+  template <typename T>
+  T get() {
+    T v{};
+    if (pos + sizeof(T) > buf.size()) {
+      ok = false;
+      return v;
+    }
+    std::memcpy(&v, buf.data() + pos, sizeof(T));
+    pos += sizeof(T);
+    return v;
+  }
+  bool bytes(void* dst, size_t n) {
+    if (pos + n > buf.size() || pos + n < pos) return ok = false;
+    if (n) std::memcpy(dst, buf.data() + pos, n);
+    pos += n;
+    return true;
+  }
+};
+
+}  // namespace
+
+struct dtq_checkpoint_s {
+  std::vector<CkptLayer> layers;
+};
+
+namespace {
+
+int parse_checkpoint(const std::vector<char>& buf, dtq_checkpoint_s* ck) {
+  static const char kMagic[8] = {'D', 'T', 'Q', 'C', 'K', 'P', 'T', '\0'};
+  CkptReader r{buf};
+  char magic[8];
+  if (!r.bytes(magic, 8) || std::memcmp(magic, kMagic, 8) != 0)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "checkpoint magic mismatch");
+  const uint16_t version = r.get<uint16_t>();
+  if (!r.ok || version != 1)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "unsupported checkpoint format version %u", version);
+  const uint32_t n = r.get<uint32_t>();
+  if (!r.ok) return fail(DTQ_ERR_INVALID_ARGUMENT, "truncated checkpoint header");
+  for (uint32_t i = 0; i < n; ++i) {
+    CkptLayer L;
+    const uint16_t name_len = r.get<uint16_t>();
+    L.name.resize(name_len);
+    if (!r.ok || !r.bytes(L.name.data(), name_len))
+      return fail(DTQ_ERR_INVALID_ARGUMENT, "truncated layer name (layer %u)", i);
+    L.N = r.get<uint32_t>();
+    L.K = r.get<uint32_t>();
+    L.bits = r.get<uint8_t>();
+    L.grouping = r.get<uint8_t>();
+    L.group_size = r.get<uint32_t>();
+    L.symmetric = r.get<uint8_t>() != 0;
+    const uint32_t n_params = r.get<uint32_t>();
+    if (!r.ok) return fail(DTQ_ERR_INVALID_ARGUMENT, "truncated layer header (layer %u)", i);
+    if (!bits_supported(L.bits))
+      return fail(DTQ_ERR_INVALID_ARGUMENT, "checkpoint with unsupported bits (%d)", L.bits);
+    L.scale.resize(n_params);
+    if (!r.bytes(L.scale.data(), 4ull * n_params))
+      return fail(DTQ_ERR_INVALID_ARGUMENT, "truncated layer params (layer %u)", i);
+    if (!L.symmetric) {
+      L.zero.resize(n_params);
+      if (!r.bytes(L.zero.data(), 4ull * n_params))
+        return fail(DTQ_ERR_INVALID_ARGUMENT, "truncated layer params (layer %u)", i);
+    }
+    const uint64_t packed_len = r.get<uint64_t>();
+    const uint64_t want = (static_cast<uint64_t>(L.N) * L.K * L.bits + 7) / 8;
+    if (!r.ok || packed_len != want)
+      return fail(DTQ_ERR_INVALID_ARGUMENT, "bad packing length (layer %u)", i);
+    L.packed.resize(packed_len);
+    if (!r.bytes(L.packed.data(), packed_len))
+      return fail(DTQ_ERR_INVALID_ARGUMENT, "truncated layer weights (layer %u)", i);
+    const uint32_t mask_len = r.get<uint32_t>();
+    L.mask.resize(r.ok ? mask_len : 0);
+    if (!r.ok || !r.bytes(L.mask.data(), 4ull * mask_len))
+      return fail(DTQ_ERR_INVALID_ARGUMENT, "truncated layer mask (layer %u)", i);
+    const uint32_t rot_len = r.get<uint32_t>();
+    if (!r.ok) return fail(DTQ_ERR_INVALID_ARGUMENT, "truncated layer rotation (layer %u)", i);
+    if (rot_len > 0) {
+      std::vector<uint8_t> bitsv((rot_len + 7) / 8);
+      if (!r.bytes(bitsv.data(), bitsv.size()))
+        return fail(DTQ_ERR_INVALID_ARGUMENT, "truncated layer rotation (layer %u)", i);
+      L.rot.resize(rot_len);
+      for (uint32_t j = 0; j < rot_len; ++j) L.rot[j] = ((bitsv[j / 8] >> (j % 8)) & 1) ? 1 : -1;
+    }
+    ck->layers.push_back(std::move(L));
+  }
+  if (r.pos != buf.size()) return fail(DTQ_ERR_INVALID_ARGUMENT, "trailing bytes after last layer");
+  return DTQ_OK;
+}
+
+}  // namespace
+
 // ================================================================== C ABI
 extern "C" {
 
@@ -986,6 +1102,112 @@ int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_
   CUDA_TRY(cudaStreamSynchronize(st));
   if (bad) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: non-finite input");
   return DTQ_OK;
+}
+
+
+int dtq_checkpoint_open(const char* path, dtq_checkpoint_t* out) {
+  if (!out || !path) return fail(DTQ_ERR_INVALID_ARGUMENT, "checkpoint_open: null argument");
+  *out = nullptr;
+  std::ifstream f(path, std::ios::binary);
+  if (!f) return fail(DTQ_ERR_INVALID_ARGUMENT, "cannot open checkpoint %s", path);
+  std::vector<char> buf((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+  auto* ck = new dtq_checkpoint_s();
+  const int r = parse_checkpoint(buf, ck);
+  if (r != DTQ_OK) {
+    delete ck;
+    return r;
+  }
+  *out = ck;
+  return DTQ_OK;
+}
+
+int dtq_checkpoint_close(dtq_checkpoint_t ck) {
+  delete ck;
+  return DTQ_OK;
+}
+
+int dtq_checkpoint_num_layers(dtq_checkpoint_t ck, int64_t* n) {
+  if (!ck || !n) return fail(DTQ_ERR_INVALID_ARGUMENT, "checkpoint: null argument");
+  *n = static_cast<int64_t>(ck->layers.size());
+  return DTQ_OK;
+}
+
+int dtq_checkpoint_layer_info(dtq_checkpoint_t ck, int64_t i, const char** name, int64_t* N,
+                              int64_t* K, int* bits, int* symmetric, int64_t* mask_len,
+                              int64_t* rot_len) {
+  if (!ck || i < 0 || i >= static_cast<int64_t>(ck->layers.size()))
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "checkpoint: bad layer index %lld", (long long)i);
+  const CkptLayer& L = ck->layers[static_cast<size_t>(i)];
+  if (name) *name = L.name.c_str();
+  if (N) *N = L.N;
+  if (K) *K = L.K;
+  if (bits) *bits = L.bits;
+  if (symmetric) *symmetric = L.symmetric ? 1 : 0;
+  if (mask_len) *mask_len = static_cast<int64_t>(L.mask.size());
+  if (rot_len) *rot_len = static_cast<int64_t>(L.rot.size());
+  return DTQ_OK;
+}
+
+int dtq_checkpoint_load_layer(dtq_checkpoint_t ck, int64_t i, int act_bits, int hblock,
+                              void* stream, dtq_qlinear_t* out) {
+  if (!out) return fail(DTQ_ERR_INVALID_ARGUMENT, "checkpoint_load_layer: null out");
+  *out = nullptr;
+  if (!ck || i < 0 || i >= static_cast<int64_t>(ck->layers.size()))
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "checkpoint: bad layer index %lld", (long long)i);
+  const CkptLayer& L = ck->layers[static_cast<size_t>(i)];
+  // the GEMM's weight layout: symmetric, one group per output channel (Grouping 3)
+  if (!L.symmetric || L.grouping != 3 || static_cast<int64_t>(L.scale.size()) != L.N)
+    return fail(DTQ_ERR_UNSUPPORTED,
+                "checkpoint layer '%s': only symmetric per-output-channel weights load "
+                "onto the tensor-core GEMM", L.name.c_str());
+  if (!L.mask.empty() && static_cast<int64_t>(L.mask.size()) != L.K)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "checkpoint layer '%s': mask length != C_in",
+                L.name.c_str());
+  if (!L.rot.empty() && static_cast<int64_t>(L.rot.size()) != L.K)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "checkpoint layer '%s': rotation length != C_in",
+                L.name.c_str());
+  DTQ_TRY(check_device());
+  cudaStream_t st = as_stream(stream);
+  std::vector<double> s(L.scale.begin(), L.scale.end());  // f32 -> f64, as read_checkpoint
+  std::vector<double> smooth(L.mask.begin(), L.mask.end());
+  uint8_t* d_codes = nullptr;
+  double* d_s = nullptr;
+  double* d_sm = nullptr;
+  int8_t* d_rot = nullptr;
+  int r = DTQ_OK;
+  auto cleanup = [&] {
+    if (d_codes) cudaFree(d_codes);
+    if (d_s) cudaFree(d_s);
+    if (d_sm) cudaFree(d_sm);
+    if (d_rot) cudaFree(d_rot);
+  };
+  if (cudaMalloc(&d_codes, L.packed.size()) != cudaSuccess ||
+      cudaMalloc(&d_s, s.size() * sizeof(double)) != cudaSuccess ||
+      (!smooth.empty() && cudaMalloc(&d_sm, smooth.size() * sizeof(double)) != cudaSuccess) ||
+      (!L.rot.empty() && cudaMalloc(&d_rot, L.rot.size()) != cudaSuccess)) {
+    cleanup();
+    return fail(DTQ_ERR_CUDA, "checkpoint_load_layer: out of device memory");
+  }
+  // the packed stream goes up as stored; the device unpacks it (W4: into the
+  // GEMM's nibble layout, no host repack)
+  if (cudaMemcpyAsync(d_codes, L.packed.data(), L.packed.size(), cudaMemcpyHostToDevice, st) !=
+          cudaSuccess ||
+      cudaMemcpyAsync(d_s, s.data(), s.size() * sizeof(double), cudaMemcpyHostToDevice, st) !=
+          cudaSuccess ||
+      (d_sm && cudaMemcpyAsync(d_sm, smooth.data(), smooth.size() * sizeof(double),
+                               cudaMemcpyHostToDevice, st) != cudaSuccess) ||
+      (d_rot && cudaMemcpyAsync(d_rot, L.rot.data(), L.rot.size(), cudaMemcpyHostToDevice, st) !=
+                    cudaSuccess)) {
+    cleanup();
+    return fail(DTQ_ERR_CUDA, "checkpoint_load_layer: upload failed");
+  }
+  dtq_balance bal{d_sm, d_rot, d_rot ? (hblock > 0 ? hblock : static_cast<int>(L.rot.size())) : 0};
+  r = dtq_qlinear_create_from_codes(d_codes, 1, 0, L.bits, d_s, L.N, L.K, act_bits, nullptr,
+                                    (d_sm || d_rot) ? &bal : nullptr, stream, out);
+  if (cudaStreamSynchronize(st) != cudaSuccess && r == DTQ_OK)
+    r = fail(DTQ_ERR_CUDA, "checkpoint_load_layer: device error");
+  cleanup();
+  return r;
 }
 
 }  // extern "C"

@@ -118,8 +118,37 @@ def main():
                      f"rag{i}_sw": sw, f"rag{i}_zw": zw, f"rag{i}_y": yy, f"rag{i}_xc": xc,
                      f"rag{i}_xs": xs_, f"rag{i}_xz": xz})
 
+    # ---- a quantized checkpoint written by the reference (trace_io.cpp) --
+    # (own RNG so the arrays above are unchanged)
+    crng = np.random.default_rng(77)
+    ck_layers = []
+    for i, (name, n, k, b, bal) in enumerate([("blocks.0.attn.qkv", 64, 256, 8, True),
+                                              ("blocks.0.mlp.fc1", 96, 256, 4, False),
+                                              ("blocks.0.mlp.fc2", 48, 128, 6, False),
+                                              ("blocks.0.attn.proj", 32, 128, 2, False)]):
+        wk = crng.standard_normal((n, k)) / np.sqrt(k)
+        mask = (np.exp(0.3 * crng.standard_normal(k))).astype(np.float32) if bal else None
+        rot = ref.hadamard_signs(k, 11) if bal else None
+        ck_layers.append((name, wk, b, mask, rot))
+    ck_path = os.path.join(os.path.dirname(OUT), "ckpt.bin")
+    ref.write_checkpoint(ck_path, ck_layers)
+    for i, (name, wk, b, mask, rot) in enumerate(ck_layers):
+        n, k = wk.shape
+        c, sc, zc = ref.read_checkpoint_layer(ck_path, i, n, k)
+        gold.update({f"ck{i}_codes": c, f"ck{i}_s": sc, f"ck{i}_z": zc})
+        if mask is not None:
+            # the layer's forward as the reference composes it: X / mask, the
+            # full K-point rotation (balance.cpp:57-67, 94-107), then
+            # qlinear_forward over the stored codes
+            xk = activations(crng, 40, k)
+            xs_, _ = ref.apply_scaling(xk.astype(np.float64), wk, mask.astype(np.float64))
+            xr_ = ref.rotate_blocks(xs_, rot, k)
+            gold.update({f"ck{i}_mask": mask, f"ck{i}_rot": rot, f"ck{i}_x": xk,
+                         f"ck{i}_y": ref.qlinear_forward(xr_, c, sc, zc, b, None)})
+
     np.savez_compressed(OUT, **gold)
-    print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes, {len(gold)} arrays)")
+    print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes, {len(gold)} arrays), {ck_path} "
+          f"({os.path.getsize(ck_path)} bytes)")
 
 
 if __name__ == "__main__":

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -48,19 +49,60 @@ void cuda(cudaError_t e) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
 }
 
+// Device buffers come from a per-thread pool of power-of-two blocks: the
+// value-semantics API makes many small calls, and cudaMalloc / cudaFree per
+// call would cost more than the kernels.
+class DevicePool {
+ public:
+  void* get(std::size_t bytes) {
+    const std::size_t b = bucket(bytes);
+    auto it = free_.find(b);
+    if (it != free_.end()) {
+      void* p = it->second;
+      free_.erase(it);
+      return p;
+    }
+    void* p = nullptr;
+    cuda(cudaMalloc(&p, b));
+    return p;
+  }
+  void put(void* p, std::size_t bytes) {
+    if (free_.size() < 256)
+      free_.emplace(bucket(bytes), p);
+    else
+      cudaFree(p);
+  }
+  ~DevicePool() {
+    for (auto& kv : free_) cudaFree(kv.second);
+  }
+
+ private:
+  static std::size_t bucket(std::size_t n) {
+    std::size_t b = 256;
+    while (b < n) b <<= 1;
+    return b;
+  }
+  std::multimap<std::size_t, void*> free_;
+};
+
+DevicePool& pool() {
+  thread_local DevicePool p;
+  return p;
+}
+
 // RAII device buffer
 template <typename T>
 struct Dev {
   T* p = nullptr;
   std::size_t n = 0;
   explicit Dev(std::size_t count) : n(count) {
-    if (n) cuda(cudaMalloc(reinterpret_cast<void**>(&p), n * sizeof(T)));
+    if (n) p = static_cast<T*>(pool().get(n * sizeof(T)));
   }
   Dev(const T* host, std::size_t count) : Dev(count) {
     if (n) cuda(cudaMemcpy(p, host, n * sizeof(T), cudaMemcpyHostToDevice));
   }
   ~Dev() {
-    if (p) cudaFree(p);
+    if (p) pool().put(p, n * sizeof(T));
   }
   Dev(const Dev&) = delete;
   Dev& operator=(const Dev&) = delete;

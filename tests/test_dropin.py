@@ -90,3 +90,21 @@ def test_reference_unit_tests_pass_on_device():
     print(r.stderr[-4000:])
     assert r.returncode == 0, r.stderr[-4000:]
     assert "0 failed" in r.stdout
+
+
+ACC = os.path.join(ROOT, "tests", "dropin", "_bin", "dtq_ref_acceptance")
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_suite_passes_on_device(tmp_path):
+    # tests/acceptance.cpp (10 criteria: quantizer correctness over 10k trials,
+    # grouping, balance invariance, incoherence, int GEMM == float path, the
+    # toy-DiT ablation ordering, memory ratios, plan arithmetic, heatmap,
+    # serialization) with the reference's own toydit / sensitivity / trace_io
+    # sources and every core numerics call on the B200 drop-in
+    if not os.path.exists(ACC):
+        pytest.skip("acceptance binary not built (needs /root/reference at build time)")
+    r = subprocess.run([ACC], capture_output=True, text=True, timeout=900, cwd=tmp_path)
+    print(r.stdout[-3000:])
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "all criteria passed" in r.stdout

@@ -102,6 +102,14 @@ __host__ __device__ inline int fq_tile_threads(int64_t K, int R) {
   return static_cast<int>((fq_lanes(K) * R * (K / 128) + 31) / 32 * 32);
 }
 
+// Per-column tables are stored pair-interleaved, (A[c], A[c + 64]) adjacent
+// for c in the first half of each 128-column block, so a lane's multiplier
+// pairs come straight out of 128-bit loads into aligned register pairs.
+__device__ __forceinline__ int fq_pair_slot(int c) {
+  const int j = c & 127;
+  return (c & ~127) + (j < 64 ? 2 * j : 2 * (j - 64) + 1);
+}
+
 __device__ __forceinline__ float max3f(float a, float b, float c) {
   float d;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
@@ -289,7 +297,7 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int c = c0 + u * blockDim.x;
-        if (c < K) colA[c] = m[u];
+        if (c < K) colA[fq_pair_slot(c)] = m[u];
       }
     }
   }
@@ -319,10 +327,10 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
         const int c = c0 + u * blockDim.x;
         if (c < K) {
           if constexpr (has_b) {
-            colA[c] = (1.f + sc[u]) * m[u];
-            colB[c] = sh[u] * m[u];
+            colA[fq_pair_slot(c)] = (1.f + sc[u]) * m[u];
+            colB[fq_pair_slot(c)] = sh[u] * m[u];
           } else {
-            colA[c] = m[u];
+            colA[fq_pair_slot(c)] = m[u];
           }
         }
       }
@@ -437,22 +445,28 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
       for (int m = 0; m < kFqRuns / 2; ++m) {
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          const int cl = c0 + 16 * kFqQ * m + 4 * g, ch = cl + 64;  // .x run and .y run
-          const float4 A0 = *reinterpret_cast<const float4*>(colA + cl);
-          const float4 A1 = *reinterpret_cast<const float4*>(colA + ch);
+          // pairs 16m + 4g .. +3: .x columns jx = 16p + 16*kQ*m + 4g + (0..3) of
+          // block b, .y columns jx + 64 -> pair slots b*64 + jx (interleaved)
+          const int base = b * 64 + 16 * p + 16 * kFqQ * m + 4 * g;
+          const float4 a01 = *reinterpret_cast<const float4*>(
+              reinterpret_cast<const float2*>(colA) + base);
+          const float4 a23 = *reinterpret_cast<const float4*>(
+              reinterpret_cast<const float2*>(colA) + base + 2);
           float2* Q = P + 16 * m + 4 * g;
           if constexpr (has_b) {
-            const float4 B0 = *reinterpret_cast<const float4*>(colB + cl);
-            const float4 B1 = *reinterpret_cast<const float4*>(colB + ch);
-            Q[0] = __ffma2_rn(Q[0], make_float2(A0.x, A1.x), make_float2(B0.x, B1.x));
-            Q[1] = __ffma2_rn(Q[1], make_float2(A0.y, A1.y), make_float2(B0.y, B1.y));
-            Q[2] = __ffma2_rn(Q[2], make_float2(A0.z, A1.z), make_float2(B0.z, B1.z));
-            Q[3] = __ffma2_rn(Q[3], make_float2(A0.w, A1.w), make_float2(B0.w, B1.w));
+            const float4 b01 = *reinterpret_cast<const float4*>(
+                reinterpret_cast<const float2*>(colB) + base);
+            const float4 b23 = *reinterpret_cast<const float4*>(
+                reinterpret_cast<const float2*>(colB) + base + 2);
+            Q[0] = __ffma2_rn(Q[0], make_float2(a01.x, a01.y), make_float2(b01.x, b01.y));
+            Q[1] = __ffma2_rn(Q[1], make_float2(a01.z, a01.w), make_float2(b01.z, b01.w));
+            Q[2] = __ffma2_rn(Q[2], make_float2(a23.x, a23.y), make_float2(b23.x, b23.y));
+            Q[3] = __ffma2_rn(Q[3], make_float2(a23.z, a23.w), make_float2(b23.z, b23.w));
           } else {
-            Q[0] = __fmul2_rn(Q[0], make_float2(A0.x, A1.x));
-            Q[1] = __fmul2_rn(Q[1], make_float2(A0.y, A1.y));
-            Q[2] = __fmul2_rn(Q[2], make_float2(A0.z, A1.z));
-            Q[3] = __fmul2_rn(Q[3], make_float2(A0.w, A1.w));
+            Q[0] = __fmul2_rn(Q[0], make_float2(a01.x, a01.y));
+            Q[1] = __fmul2_rn(Q[1], make_float2(a01.z, a01.w));
+            Q[2] = __fmul2_rn(Q[2], make_float2(a23.x, a23.y));
+            Q[3] = __fmul2_rn(Q[3], make_float2(a23.z, a23.w));
           }
         }
       }
@@ -488,10 +502,10 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
       else
         stage(16);  // element stride 32 (local stride 16)
 #pragma unroll
-      for (int k = 0; k < kFqPairs; ++k) {  // element stride 64: inside each pair
-        const float u = P[k].x, w = P[k].y;
-        P[k] = make_float2(u + w, u - w);
-      }
+      for (int k = 0; k < kFqPairs; ++k)  // element stride 64: inside each pair, one
+        // FFMA2 with both operands broadcast: (x + y, x - y) = y*(1, -1) + x
+        P[k] = __ffma2_rn(make_float2(P[k].y, P[k].y), make_float2(1.f, -1.f),
+                          make_float2(P[k].x, P[k].x));
     }
     if (a.status != nullptr && ok) {
       // non-finite input <=> non-finite sum (after the transform P[0].x of

@@ -358,3 +358,18 @@ def test_tile_quantizer_varying_tile_heights_in_one_process():
         x = torch.randn(M, K, device=DEV).half()
         codes, s, z = dtq.quantize_rows(x, balance=bal)
         assert codes.shape == (M, K) and bool(torch.isfinite(s).all())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("K", [1152, 4608, 8192])
+def test_quantizer_input_dtypes_wide_rows(oracle, dtype, K):
+    # tile kernel (two lanes per block beyond K = 1152, four-row tiles beyond
+    # 4608) and, for fp32 rows too wide for a shared-memory tile, the
+    # lane-group kernel: codes / s / z bit-exact with no balance
+    rng = np.random.default_rng(K + 3)
+    x = torch.from_numpy((rng.standard_normal((70, K)) * 3).astype(np.float32)).to(dtype)
+    codes, s, z = dtq.quantize_rows(x.to(DEV))
+    c_ref, s_ref, z_ref = oracle.quantize_rows(x.double().numpy(), 8)
+    assert np.array_equal(codes.cpu().numpy(), c_ref)
+    assert np.array_equal(s.cpu().numpy(), s_ref) and np.array_equal(z.cpu().numpy(), z_ref)

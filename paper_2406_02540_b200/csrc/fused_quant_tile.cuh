@@ -388,6 +388,22 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
       }
     }
 
+    if (a.dbg == 3) {  // diagnostics: the memory pipeline alone (raw bits out, no math)
+      if (ok) {
+        uint8_t* dst = a.codes + row * a.ldc + c0;
+#pragma unroll
+        for (int m = 0; m < kFqRuns; ++m) {
+          const float2* Q = P + 16 * (m % (kFqRuns / 2));
+          *reinterpret_cast<uint4*>(dst + 16 * kFqQ * m) =
+              make_uint4(__float_as_uint(Q[0].x) ^ __float_as_uint(Q[1].y),
+                         __float_as_uint(Q[2].x) ^ __float_as_uint(Q[3].y),
+                         __float_as_uint(Q[4].x) ^ __float_as_uint(Q[5].y),
+                         __float_as_uint(Q[6].x) ^ __float_as_uint(Q[7].y));
+        }
+      }
+      __syncthreads();
+      continue;
+    }
     // ---- 2. prologue
     if constexpr (kPro == kProGelu) {
 #pragma unroll
@@ -440,7 +456,7 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
     }
 
     // ---- 3. folded column map, then the transform
-    if (has_a) {
+    if (has_a && a.dbg != 4) {
 #pragma unroll
       for (int m = 0; m < kFqRuns / 2; ++m) {
 #pragma unroll
@@ -471,7 +487,7 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
         }
       }
     }
-    if (kRot && a.dbg != 1) {
+    if (kRot && a.dbg != 1 && a.dbg != 4) {
       const float2 neg = make_float2(-1.f, -1.f);
       auto stage = [&](int h) {  // local stride h over the pair index
 #pragma unroll
@@ -496,9 +512,10 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
           P[k] = __ffma2_rn(P[k], sg, make_float2(ox, oy));
         }
       };
-      xlane(kFqItems, sg16);  // element stride 16
-      if constexpr (kFqQ == 4)
-        xlane(2 * kFqItems, sg32);  // element stride 32
+      if (a.dbg != 5) xlane(kFqItems, sg16);  // element stride 16
+      if constexpr (kFqQ == 4) {
+        if (a.dbg != 5) xlane(2 * kFqItems, sg32);  // element stride 32
+      }
       else
         stage(16);  // element stride 32 (local stride 16)
 #pragma unroll

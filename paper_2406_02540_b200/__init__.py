@@ -25,7 +25,7 @@ from dataclasses import dataclass
 from typing import Optional
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdtq_b200.so")
+LIB_PATH = os.environ.get("DTQ_B200_LIB") or os.path.join(HERE, "libdtq_b200.so")  # override: diagnostics builds
 
 F16, BF16, F32, F64, S32 = 0, 1, 2, 3, 4
 MODE_FAST, MODE_EXACT = 0, 1

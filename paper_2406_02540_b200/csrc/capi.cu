@@ -423,12 +423,14 @@ struct dtq_qlinear_s {
   void* hy = nullptr;
   size_t hy_bytes = 0;
   int32_t* status = nullptr;
-  // host-forward pipeline: two streams alternate row chunks (H2D, quantize +
-  // GEMM, D2H), each with its own workspace
-  cudaStream_t ps[2] = {nullptr, nullptr};
-  cudaEvent_t pe[3] = {nullptr, nullptr, nullptr};
-  void* pws[2] = {nullptr, nullptr};
-  size_t pws_bytes[2] = {0, 0};
+  // host-forward pipeline over row chunks: one stream per role (H2D copies,
+  // quantize + GEMM, D2H copies) chained per chunk by events, so the copy
+  // engines in the two directions never wait on each other's queue
+  cudaStream_t ps[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t pe[2] = {nullptr, nullptr};          // fork / join
+  std::vector<cudaEvent_t> ev_in, ev_out;          // per chunk: H2D done, GEMM done
+  void* pws = nullptr;
+  size_t pws_bytes = 0;
 };
 
 namespace {
@@ -448,12 +450,13 @@ void free_handle(dtq_qlinear_s* h) {
                   h->col_mul, h->signs, h->scratch, h->acc32, h->hx, h->hy, h->status};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  for (int i = 0; i < 2; ++i) {
-    if (h->pws[i]) cudaFree(h->pws[i]);
-    if (h->ps[i]) cudaStreamDestroy(h->ps[i]);
-  }
+  if (h->pws) cudaFree(h->pws);
+  for (cudaStream_t s : h->ps)
+    if (s) cudaStreamDestroy(s);
   for (cudaEvent_t e : h->pe)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->ev_in) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->ev_out) cudaEventDestroy(e);
   delete h;
 }
 
@@ -1053,12 +1056,18 @@ int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_
   DTQ_TRY(grow(&h->hx, &h->hx_bytes, xb));
   DTQ_TRY(grow(&h->hy, &h->hy_bytes, yb));
   CUDA_TRY(cudaMemsetAsync(h->status, 0, sizeof(int32_t), st));
-  // Row chunks (>= 256 rows, ~8 of them) pipelined over two streams so the
-  // H2D of chunk i+1 and the D2H of chunk i-1 overlap chunk i's kernels
-  // (quantization is row-local, so chunks are independent).  The F64 parity
-  // output uses a handle-wide s32 scratch and stays in one piece.
-  int64_t chunk = (M + 7) / 8;
-  chunk = (chunk + 255) / 256 * 256;
+  // Row chunks (~8 of them, multiples of 128 rows) in a three-stage pipeline:
+  // H2D on one stream, quantize + GEMM of chunk i once its rows have landed,
+  // D2H of chunk i once its GEMM is done, on a third stream (quantization is row-local, so chunks are independent).
+  // The D2H (the larger transfer: N > K columns) then runs back to back from
+  // the first chunk on.  The F64 parity output uses a handle-wide s32
+  // scratch and stays in one piece.
+  static const int nchunks = [] {  // DTQ_HOST_CHUNKS (diagnostics): pipeline depth
+    const char* e = std::getenv("DTQ_HOST_CHUNKS");
+    return e && std::atoi(e) > 0 ? std::atoi(e) : 8;
+  }();
+  int64_t chunk = (M + nchunks - 1) / nchunks;
+  chunk = (chunk + 127) / 128 * 128;
   if (y_dtype == DTQ_F64 || M < 1024) chunk = M;
   if (chunk >= M) {
     CUDA_TRY(cudaMemcpyAsync(h->hx, x, xb, cudaMemcpyHostToDevice, st));
@@ -1069,33 +1078,78 @@ int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_
     int64_t ldc;
     size_t a_, b_;
     const size_t wsb = ws_layout(h, chunk, &ldc, &a_, &b_);
-    for (int i = 0; i < 2; ++i) {
-      if (!h->ps[i]) CUDA_TRY(cudaStreamCreateWithFlags(&h->ps[i], cudaStreamNonBlocking));
-      DTQ_TRY(grow(&h->pws[i], &h->pws_bytes[i], wsb));
+    DTQ_TRY(grow(&h->pws, &h->pws_bytes, wsb));
+    for (cudaStream_t& s : h->ps)
+      if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : h->pe)
+      if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const size_t nc = static_cast<size_t>((M + chunk - 1) / chunk);
+    while (h->ev_in.size() < nc) {
+      cudaEvent_t a, b;
+      CUDA_TRY(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      h->ev_in.push_back(a);
+      h->ev_out.push_back(b);
     }
-    for (int i = 0; i < 3; ++i)
-      if (!h->pe[i]) CUDA_TRY(cudaEventCreateWithFlags(&h->pe[i], cudaEventDisableTiming));
-    CUDA_TRY(cudaEventRecord(h->pe[0], st));
-    CUDA_TRY(cudaStreamWaitEvent(h->ps[0], h->pe[0], 0));
-    CUDA_TRY(cudaStreamWaitEvent(h->ps[1], h->pe[0], 0));
-    int c = 0;
+    cudaStream_t s_in = h->ps[0], s_cmp = h->ps[1], s_out = h->ps[2];
+    // DTQ_HOST_TRACE=1 (diagnostics): per-chunk stage completion times to stderr
+    static const bool trace = [] {
+      const char* e = std::getenv("DTQ_HOST_TRACE");
+      return e && e[0] == '1';
+    }();
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t s) {
+      if (!trace) return;
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, s);
+      tev.push_back(e);
+    };
+    mark(st);
+    CUDA_TRY(cudaEventRecord(h->pe[0], st));  // fork: after the status reset
+    for (cudaStream_t s : h->ps) CUDA_TRY(cudaStreamWaitEvent(s, h->pe[0], 0));
+    size_t c = 0;
     for (int64_t r0 = 0; r0 < M; r0 += chunk, ++c) {
       const int64_t m = M - r0 < chunk ? M - r0 : chunk;
-      cudaStream_t s = h->ps[c & 1];
       const size_t xo = xe * static_cast<size_t>(r0) * h->K, yo = ye * static_cast<size_t>(r0) * h->N;
       uint8_t* dx = static_cast<uint8_t*>(h->hx) + xo;
       uint8_t* dy = static_cast<uint8_t*>(h->hy) + yo;
-      CUDA_TRY(cudaMemcpyAsync(dx, static_cast<const uint8_t*>(x) + xo, xe * m * h->K,
-                               cudaMemcpyHostToDevice, s));
-      DTQ_TRY(forward_impl(dx, x_dtype, m, h->K, h, mode, nullptr, dy, y_dtype, h->N,
-                           h->pws[c & 1], h->pws_bytes[c & 1], h->status, s));
+      // H2D in three pieces: chunk 0, chunk 1, then everything else as one
+      // copy.  Interleaving many small H2D copies with the D2H stream costs
+      // ~12% of the D2H rate on PCIe; the first two small pieces start the
+      // pipeline, the large one lands while chunks 0-1 drain.
+      if (c <= 2) {
+        const int64_t rows = c < 2 ? m : M - r0;
+        CUDA_TRY(cudaMemcpyAsync(dx, static_cast<const uint8_t*>(x) + xo, xe * rows * h->K,
+                                 cudaMemcpyHostToDevice, s_in));
+        CUDA_TRY(cudaEventRecord(h->ev_in[c], s_in));
+        mark(s_in);
+      }
+      CUDA_TRY(cudaStreamWaitEvent(s_cmp, h->ev_in[c < 2 ? c : 2], 0));
+      DTQ_TRY(forward_impl(dx, x_dtype, m, h->K, h, mode, nullptr, dy, y_dtype, h->N, h->pws,
+                           h->pws_bytes, h->status, s_cmp));
+      CUDA_TRY(cudaEventRecord(h->ev_out[c], s_cmp));
+      mark(s_cmp);
+      CUDA_TRY(cudaStreamWaitEvent(s_out, h->ev_out[c], 0));
       CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(y) + yo, dy, ye * m * h->N,
-                               cudaMemcpyDeviceToHost, s));
+                               cudaMemcpyDeviceToHost, s_out));
+      mark(s_out);
     }
-    CUDA_TRY(cudaEventRecord(h->pe[1], h->ps[0]));
-    CUDA_TRY(cudaEventRecord(h->pe[2], h->ps[1]));
+    // join: the D2H stream finishes last (it waits on every GEMM, which waits
+    // on every H2D)
+    CUDA_TRY(cudaEventRecord(h->pe[1], s_out));
     CUDA_TRY(cudaStreamWaitEvent(st, h->pe[1], 0));
-    CUDA_TRY(cudaStreamWaitEvent(st, h->pe[2], 0));
+    if (trace) {
+      cudaStreamSynchronize(st);
+      std::string line = "forward_host trace (us from fork; in/gemm/out per chunk):";
+      for (size_t k = 1; k < tev.size(); ++k) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, tev[0], tev[k]);
+        line += " " + std::to_string(static_cast<int>(ms * 1e3f));
+      }
+      fprintf(stderr, "%s\n", line.c_str());
+      for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
   }
   int32_t bad = 0;
   CUDA_TRY(cudaMemcpyAsync(&bad, h->status, sizeof(int32_t), cudaMemcpyDeviceToHost, st));

@@ -61,9 +61,12 @@ constexpr int BK = 128;  // bytes (= int8 elements) per k-block: one 128-byte sw
 constexpr int kConvWarps = 4;
 // epilogue warps: 8 for W8A8 (two per TMEM lane quarter, each half of the
 // columns); 4 for W4A8, whose 4 converter warps take the remaining slots.
+#ifndef DTQ_W8_EPI_WARPS
+#define DTQ_W8_EPI_WARPS 8
+#endif
 template <bool kW4>
 __host__ __device__ constexpr int epi_warps() {
-  return kW4 ? 4 : 8;
+  return kW4 ? 4 : DTQ_W8_EPI_WARPS;
 }
 
 template <int BN, int kStages, bool kW4, bool k2Cta = false>
@@ -72,7 +75,7 @@ struct Smem {
   static constexpr int kBRows = k2Cta ? BN / 2 : BN;   // a CTA pair splits B along N
   static constexpr int kB = kBRows * BK;               // s8 tile
   static constexpr int kP = kW4 ? kBRows * (BK / 2) : 0;  // packed nibbles (this CTA's rows)
-  static constexpr int kEpiBufs = 2;                             // staging buffers per warp
+  static constexpr int kEpiBufs = epi_warps<kW4>() > 8 ? 1 : 2;  // staging buffers per warp
   static constexpr int kEpi = epi_warps<kW4>() * kEpiBufs * 32 * 64;  // 32 rows x 64 B each
   static constexpr int kPar = 2 * 3 * BN * 4;             // {s_w, wsum, bias} x 2 tiles
   static constexpr int offA = 0;
@@ -358,14 +361,22 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       // TMEM -> registers, 32 columns at a time; chunk cl+1 is in flight while
       // chunk cl is dequantised and stored (two register sets, full unroll)
       const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * BN + cgrp * kCols;
-      uint32_t rr[2][32];
+      // (16 epilogue warps: one register set -- the other warps hide the
+      // load latency, and 576 threads leave ~100 registers each)
+      constexpr int kLdSets = kEpiWarps > 8 ? 1 : 2;
+      uint32_t rr[kLdSets][32];
       tmem_ld_32x32b_x32(tbase, rr[0]);
       tmem_ld_wait_regs(rr[0]);
 #pragma unroll
       for (int cl = 0; cl < kCols / 32; ++cl) {
         const int c = cgrp * (kCols / 32) + cl;  // 32-column chunk index within the tile
-        uint32_t (&r)[32] = rr[cl & 1];
-        if (cl + 1 < kCols / 32) tmem_ld_32x32b_x32(tbase + (cl + 1) * 32, rr[(cl + 1) & 1]);
+        uint32_t (&r)[32] = rr[cl % kLdSets];
+        if (kLdSets == 1 && cl > 0) {
+          tmem_ld_32x32b_x32(tbase + cl * 32, r);
+          tmem_ld_wait_regs(r);
+        }
+        if (kLdSets == 2 && cl + 1 < kCols / 32)
+          tmem_ld_32x32b_x32(tbase + (cl + 1) * 32, rr[(cl + 1) % kLdSets]);
         if (cl == kCols / 32 - 1) {
           // every TMEM read of this accumulator has completed: hand it back
           tc_fence_before();
@@ -378,7 +389,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
           }
         }
         if (kOut == kOutNone || g.dbg == 2) {
-          if (cl + 1 < kCols / 32) tmem_ld_wait_regs(rr[(cl + 1) & 1]);
+          if (kLdSets == 2 && cl + 1 < kCols / 32) tmem_ld_wait_regs(rr[(cl + 1) % kLdSets]);
           continue;
         }
 #pragma unroll
@@ -513,7 +524,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
             __syncwarp();
           }
         }
-        if (cl + 1 < kCols / 32) tmem_ld_wait_regs(rr[(cl + 1) & 1]);
+        if (kLdSets == 2 && cl + 1 < kCols / 32) tmem_ld_wait_regs(rr[(cl + 1) % kLdSets]);
       }
     }
     if (g.tma_store && lane == 0) bulk_wait<0>();

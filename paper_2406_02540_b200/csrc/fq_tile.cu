@@ -14,15 +14,15 @@ int dtq_fq_tile_rows(int64_t M, int64_t K, int es, bool has_a, bool has_b, int s
   (void)M;
   (void)sms;
   constexpr size_t kMax = 220 * 1024;
-  const int cap = dtq_fq::fq_lanes(K) == 4 ? 288 : 576;  // the kernels' launch bounds
+  const bool four = dtq_fq::fq_lanes(K) == 4;
+  const int cap = four ? 288 : 576;  // the kernels' launch bounds
   static const int force = [] {  // DTQ_FQ_ROWS (diagnostics): start the search at R
     const char* e = std::getenv("DTQ_FQ_ROWS");
     return e ? std::atoi(e) : 8;
   }();
-  for (int R = force; R >= 4; R -= 4)
-    if (dtq_fq::fq_tile_threads(K, R) <= cap &&
-        dtq_fq::fq_tile_layout(K, R, es, has_a, has_b, 2).bytes <= kMax &&
-        (R == 8 || dtq_fq::fq_lanes(K) == 2))
+  for (int R = force; R >= 4; R /= 2)
+    if ((R == 8 || !four) && dtq_fq::fq_tile_threads(K, R) <= cap &&
+        dtq_fq::fq_tile_layout(K, R, es, has_a, has_b, 2).bytes <= kMax)
       return R;
   return 0;
 }

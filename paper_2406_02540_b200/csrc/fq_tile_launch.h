@@ -42,8 +42,8 @@ inline cudaError_t fq_tile_occupancy(const void* kern, int block, size_t smem, i
 
 template <typename Tin, bool kRot, bool kExactV, int kPro>
 cudaError_t launch_tile(const dtq_fq::FqArgs& a, int R, int nbuf, int sms, cudaStream_t st) {
-  // K <= 1152: 4 lanes per block, 8-row tiles (288 threads); K <= 4608: 2
-  // lanes, 8 rows (576 threads); wider: 2 lanes, 4 rows
+  // K <= 1152: 4 lanes per block, 8-row tiles (288 threads); wider: 2 lanes
+  // per block, 8 or 4 rows (576 threads)
   const bool wide = dtq_fq::fq_lanes(a.K) == 2;
   auto kern = !wide ? dtq_fq::fq_tile_kernel<Tin, kRot, kExactV, kPro, false, 8>
               : (R == 8 ? dtq_fq::fq_tile_kernel<Tin, kRot, kExactV, kPro, true, 8>

@@ -97,6 +97,8 @@ __device__ __forceinline__ float gelu1(float x) {
   return fmaf(ax, e * gelu_nerfcx_poly(u), fmaxf(x, 0.f));  // max(x,0) - |x| E
 }
 
+// (a packed FMUL2 / FFMA2-immediate formulation compiles back to these
+// scalar FFMA-immediate forms: ptxas splits it)
 __device__ __forceinline__ float2 gelu2(float2 x) { return make_float2(gelu1(x.x), gelu1(x.y)); }
 
 // ------------------------------------------------------------------ loads
@@ -370,7 +372,7 @@ __global__ void __launch_bounds__(kCPT == 1 ? 1024 : 256) fq_kernel(const FqArgs
           if constexpr (kExact)
             v[i][e] = 0.5 * v[i][e] * (1.0 + erf(v[i][e] / 1.4142135623730951));
           else
-            v[i][e] = gelu2(make_float2(static_cast<float>(v[i][e]), 0.f)).x;
+            v[i][e] = gelu1(static_cast<float>(v[i][e]));
         }
     }
 

@@ -58,22 +58,20 @@ struct FqShape {
   static constexpr int kRuns = kE / 16;    // 16-column runs
   static constexpr int kItems = 32 / kQ;   // (row, block) items per warp
 };
-// DTQ_FQ_WIDE_K (diagnostics) moves the two-lane threshold; default 1152
-// (four lanes x 8 rows x nb blocks must stay within 288 threads)
+// Four lanes per 128-column block (8-row tiles, 288-thread CTAs, two per
+// SM) up to K = 1152; wider rows use two lanes per block in 576-thread CTAs.
+// (Four lanes with shorter tiles for wider rows -- R = 4 / 2 / 1 -- measured
+// slower: 109 vs 82 us at 16384 x 4608.)  DTQ_FQ_WIDE_K (diagnostics) moves
+// the threshold.
+constexpr int64_t kFqWideK = 1152;
 __host__ inline int64_t fq_wide_k() {
   static const int64_t v = [] {
     const char* e = std::getenv("DTQ_FQ_WIDE_K");
-    return e ? static_cast<int64_t>(std::atoll(e)) : int64_t{1152};
+    return e ? static_cast<int64_t>(std::atoll(e)) : kFqWideK;
   }();
   return v;
 }
-__host__ __device__ inline int fq_lanes(int64_t K) {
-#ifdef __CUDA_ARCH__
-  return K <= 1152 ? 4 : 2;
-#else
-  return K <= fq_wide_k() ? 4 : 2;
-#endif
-}
+__host__ inline int fq_lanes(int64_t K) { return K <= fq_wide_k() ? 4 : 2; }
 
 constexpr int kFqMaxBuf = 4;  // input ring depth limit
 
@@ -98,7 +96,7 @@ __host__ __device__ inline TileLayout fq_tile_layout(int64_t K, int R, int es, b
   return L;
 }
 
-__host__ __device__ inline int fq_tile_threads(int64_t K, int R) {
+__host__ inline int fq_tile_threads(int64_t K, int R) {
   return static_cast<int>((fq_lanes(K) * R * (K / 128) + 31) / 32 * 32);
 }
 
@@ -225,10 +223,18 @@ __device__ __forceinline__ void fq_tile_codes(const float2 (&P)[FqShape<kQ>::kPa
         make_uint4(w[4 * m], w[4 * m + 1], w[4 * m + 2], w[4 * m + 3]);
 }
 
+// CTAs per SM the 288-thread kernels are register-capped for: two (112
+// registers, 18 warps per SM).  Three (72 registers) spills in the LayerNorm
+// and exact-code variants and measured slower everywhere at 16384 x 1152:
+// no prologue 22.5 vs 23.3 us, modulate 24.4 vs 27.1, LayerNorm 33.1 vs
+// 38.7, exact codes 20.7 vs 21.8.  DTQ_FQ_MINB (diagnostics build) sets it.
+#ifndef DTQ_FQ_MINB
+#define DTQ_FQ_MINB 2
+#endif
 // kWide: 576-thread CTAs (K > 1152, one per SM); otherwise <= 288 threads
-// with registers capped for three CTAs per SM
+// with registers capped for DTQ_FQ_MINB CTAs per SM
 template <typename Tin, bool kRot, bool kExactV, int kPro, bool kWide, int kR>
-__global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
+__global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
     fq_tile_kernel(const FqArgs a) {
   // compile-time tile height and ring depth: the index arithmetic folds
   constexpr int R = kR;
@@ -437,16 +443,39 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
         lM2 = lM2 + oM2 + d * d * (0.5f * n);
         n *= 2.f;
       }
-      float2* red_ln = reinterpret_cast<float2*>(red_s1);  // (mean, M2) per (block, row)
-      if (p == 0 && active) red_ln[b * R + r] = make_float2(lm, lM2);
+      // rows shorter than a warp's items (R < kFqItems): fold the warp's
+      // other blocks of the same row first (count-aware: items past the
+      // last block carry no data), so the cross-warp merge reads one
+      // partial per warp, not one per block
+      float ln_n = active ? 128.f : 0.f;
+#pragma unroll
+      for (int o = R; o < kFqItems; o <<= 1) {
+        const float om = __shfl_xor_sync(0xffffffffu, lm, o);
+        const float oM2 = __shfl_xor_sync(0xffffffffu, lM2, o);
+        const float on = __shfl_xor_sync(0xffffffffu, ln_n, o);
+        const float nn = ln_n + on;
+        const float inv = nn > 0.f ? __frcp_rn(nn) : 0.f;
+        const float d = om - lm;
+        lm = fmaf(d, on * inv, lm);
+        lM2 = lM2 + oM2 + d * d * (ln_n * on * inv);
+        ln_n = nn;
+      }
+      float2* red_ln = reinterpret_cast<float2*>(red_s1);  // (mean, M2) per (warp, row)
+      if (lane < R) red_ln[warp * R + r] = make_float2(lm, lM2);
       __syncthreads();
+      // warp j holds blocks [j*kBpw, (j+1)*kBpw) of the row
+      constexpr int kBpw = kFqItems / R;
       float2 st = red_ln[r];
-      for (int j = 1; j < nb; ++j) {
+      float st_n = 128.f * static_cast<float>(min(kBpw, nb));
+      const int nw = (nb + kBpw - 1) / kBpw;
+      for (int j = 1; j < nw; ++j) {
         const float2 o = red_ln[j * R + r];
+        const float on = 128.f * static_cast<float>(min(kBpw, nb - j * kBpw));
         const float d = o.x - st.x;
-        const float inv = __frcp_rn(static_cast<float>(j + 1));
-        st.x = fmaf(d, inv, st.x);
-        st.y = st.y + o.y + d * d * (128.f * static_cast<float>(j) * inv);
+        const float inv = __frcp_rn(st_n + on);
+        st.x = fmaf(d, on * inv, st.x);
+        st.y = st.y + o.y + d * d * (st_n * on * inv);
+        st_n += on;
       }
       const float mean = st.x;
       const float rstd = rsqrtf(st.y / static_cast<float>(K) + a.eps);
@@ -567,7 +596,14 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
         mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       }
-      if (p == 0 && active) red_mm[((it & 1) * nb + b) * R + r] = make_float2(mn, mx);
+      // R < kFqItems: the warp's other blocks of the same row (items past the
+      // last block hold a copy of block 0 of their row: harmless here)
+#pragma unroll
+      for (int o = R; o < kFqItems; o <<= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      if (lane < R) red_mm[((it & 1) * nb + warp) * R + r] = make_float2(mn, mx);
     }
     {
       const long long b0 = probe ? clock64() : 0;
@@ -576,7 +612,8 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : 3)
     }
     if (!ok) continue;
     float mn = __int_as_float(0x7f800000), mx = -mn;
-    for (int j = 0; j < nb; ++j) {
+    const int nwarp = (nb * R + kFqItems - 1) / kFqItems;  // one partial per warp
+    for (int j = 0; j < nwarp; ++j) {
       const float2 m = red_mm[((it & 1) * nb + j) * R + r];
       mn = fminf(mn, m.x);
       mx = fmaxf(mx, m.y);

@@ -21,7 +21,7 @@ int dtq_fq_tile_rows(int64_t M, int64_t K, int es, bool has_a, bool has_b, int s
     return e ? std::atoi(e) : 8;
   }();
   for (int R = force; R >= 4; R /= 2)
-    if ((R == 8 || !four) && dtq_fq::fq_tile_threads(K, R) <= cap &&
+    if ((four ? R == 8 : R >= 4) && dtq_fq::fq_tile_threads(K, R) <= cap &&
         dtq_fq::fq_tile_layout(K, R, es, has_a, has_b, 2).bytes <= kMax)
       return R;
   return 0;

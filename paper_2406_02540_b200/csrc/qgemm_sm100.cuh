@@ -316,24 +316,33 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     // in a double-buffered smem table: their global latency never stalls the
     // drain of TMEM.
     constexpr int kParPer = (BN + 32 * kEpiWarps - 1) / (32 * kEpiWarps);
-    uint32_t p_sw[kParPer], p_ws[kParPer], p_b[kParPer];
-    float nsx = 0.f;
+    // The loads are unconditional (indices clamped into range) and their
+    // values are used only when parked at the top of the next tile: any
+    // select, negate or convert right after the load would make the warp
+    // wait out the global latency before draining the current tile.
+    uint32_t p_sw[kParPer], p_b[kParPer];
+    int32_t p_ws[kParPer];
+    uint32_t p_ok = 0;  // bit i: column i is inside the tile and N; bit 31: row < M
+    double nsx = 0.0;
     int32_t nzx = 0;
     auto fetch = [&](int t) {
       const int tm0 = (t % g.tiles_m) * kTileM + rank * BM;
       const int tn0 = (t / g.tiles_m) * BN;
+      p_ok = 0;
 #pragma unroll
       for (int i = 0; i < kParPer; ++i) {
         const int col = tn0 + et + i * 32 * kEpiWarps;
         const bool okc = col < g.N && et + i * 32 * kEpiWarps < BN;
-        p_sw[i] = __float_as_uint(okc ? __ldg(g.s_w + col) : 0.f);
-        // W4: the unpacked weights are 16*w (s4x8_to_s8x8_x16), so is their sum
-        p_ws[i] = static_cast<uint32_t>(okc ? -__ldg(g.wsum + col) * (kW4 ? 16 : 1) : 0);
-        p_b[i] = __float_as_uint((okc && g.bias) ? __ldg(g.bias + col) : 0.f);
+        const int cc = min(col, g.N - 1);
+        p_ok |= okc ? (1u << i) : 0u;
+        p_sw[i] = __float_as_uint(__ldg(g.s_w + cc));
+        p_ws[i] = __ldg(g.wsum + cc);
+        p_b[i] = has_bias ? __float_as_uint(__ldg(g.bias + cc)) : 0u;
       }
       const int row = tm0 + q * 32 + lane;
-      nsx = row < g.M ? static_cast<float>(__ldg(g.s_x + row)) * (kW4 ? 0.0625f : 1.f) : 0.f;
-      nzx = row < g.M ? __ldg(g.z_x + row) : 0;
+      p_ok |= row < g.M ? (1u << 31) : 0u;
+      nsx = __ldg(g.s_x + min(row, g.M - 1));
+      nzx = __ldg(g.z_x + min(row, g.M - 1));
     };
     if (tile0 < total_tiles) fetch(tile0);
     for (int tile = tile0; tile < total_tiles; tile += tstride, ++it) {
@@ -346,13 +355,16 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       for (int i = 0; i < kParPer; ++i) {
         const int c = et + i * 32 * kEpiWarps;
         if (c < BN) {
-          par[c] = p_sw[i];
-          par[BN + c] = p_ws[i];
-          par[2 * BN + c] = p_b[i];
+          const bool okc = (p_ok >> i) & 1u;
+          par[c] = okc ? p_sw[i] : 0u;
+          // W4: the unpacked weights are 16*w (s4x8_to_s8x8_x16), so is their sum
+          par[BN + c] = okc ? static_cast<uint32_t>(-p_ws[i] * (kW4 ? 16 : 1)) : 0u;
+          par[2 * BN + c] = okc ? p_b[i] : 0u;
         }
       }
-      const float sx = nsx;
-      const int32_t zx = nzx;
+      const bool rok = p_ok >> 31;
+      const float sx = rok ? static_cast<float>(nsx) * (kW4 ? 0.0625f : 1.f) : 0.f;
+      const int32_t zx = rok ? nzx : 0;
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
       if (tile + tstride < total_tiles) fetch(tile + tstride);
 

@@ -661,6 +661,8 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
   }();
   g.dbg = dbg;
   g.probe = probe_buffer();
+  g.w4 = h->w4;
+  g.ld4 = h->ld4;
   static const bool no_tma_store = [] {
     const char* e = std::getenv("DTQ_DEBUG_NO_TMA_STORE");
     return e && e[0] == '1';

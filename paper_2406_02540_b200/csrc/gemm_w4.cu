@@ -1,14 +1,17 @@
-// gemm_w4.cu -- W4A8 instantiations (packed nibbles unpacked in smem).
+// gemm_w4.cu -- W4A8 instantiations (packed nibbles unpacked to s8 in smem).
 #include "launch.h"
 
 cudaError_t dtq_launch_gemm_w4(const CUtensorMap& tA, const CUtensorMap& tB,
                                const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, GemmCfg c,
                                int sms, cudaStream_t st) {
-  // TMA ring per stage: 16 KB A + packed nibbles of this CTA's B rows;
-  // unpacked s8 B tiles in a separate 3-deep ring
+  // unpacked s8 B tiles in a 3-deep ring of their own; the TMA stage ring
+  // holds A (+ the packed nibbles of this CTA's B rows for CTA pairs)
+  // (8 epilogue warps double the staging buffers: one stage fewer at BN=256)
+  constexpr int kS256 = dtq_gemm::epi_warps<true>() > 4 ? 5 : 6;
   if (c.cta2)  // CTA pair: each SM unpacks only its half of B
-    return c.bn == 256 ? dtq_launch_gemm_o<256, 6, true, true>(tA, tB, tY, g, sms, st)
+    return c.bn == 256 ? dtq_launch_gemm_o<256, kS256, true, true>(tA, tB, tY, g, sms, st)
                        : dtq_launch_gemm_o<128, 8, true, true>(tA, tB, tY, g, sms, st);
-  return c.bn == 256 ? dtq_launch_gemm_o<256, 3, true, false>(tA, tB, tY, g, sms, st)
-                     : dtq_launch_gemm_o<128, 6, true, false>(tA, tB, tY, g, sms, st);
+  // single CTA: the stage ring holds A only (converters read packed B from L2)
+  return c.bn == 256 ? dtq_launch_gemm_o<256, kS256, true, false>(tA, tB, tY, g, sms, st)
+                     : dtq_launch_gemm_o<128, 8, true, false>(tA, tB, tY, g, sms, st);
 }

@@ -54,19 +54,29 @@ struct GemmArgs {
   unsigned long long* probe;  // diagnostics: per-CTA wait-cycle counters (or nullptr)
   int dbg;              // diagnostics: 0 full epilogue, 2 TMEM loads only,
                         // 3 loads + dequant math, 4 + smem staging (no stores)
+  const uint8_t* w4;    // W4A8 single-CTA tiles: packed nibbles [N, ld4] (read by the
+  int64_t ld4;          // converter warps straight from L2)
 };
 
 constexpr int BM = 128;
 constexpr int BK = 128;  // bytes (= int8 elements) per k-block: one 128-byte swizzle atom
-constexpr int kConvWarps = 4;
-// epilogue warps: 8 for W8A8 (two per TMEM lane quarter, each half of the
-// columns); 4 for W4A8, whose 4 converter warps take the remaining slots.
+#ifndef DTQ_CONV_WARPS
+#define DTQ_CONV_WARPS 8
+#endif
+constexpr int kConvWarps = DTQ_CONV_WARPS;
+// epilogue warps: 8 (two per TMEM lane quarter, each half of the columns);
+// W4A8 adds 8 nibble-converter warps.  Measured at fc1 (16384 x 4608 x 1152):
+// W8A8 with 4 / 8 / 16 epilogue warps 127 / 72 / 72 us; W4A8 with 4 / 8 / 16
+// converters 164 / 140 / 226 us, and 8 epilogue warps on top 133 us.
 #ifndef DTQ_W8_EPI_WARPS
 #define DTQ_W8_EPI_WARPS 8
 #endif
+#ifndef DTQ_W4_EPI_WARPS
+#define DTQ_W4_EPI_WARPS 8
+#endif
 template <bool kW4>
 __host__ __device__ constexpr int epi_warps() {
-  return kW4 ? 4 : DTQ_W8_EPI_WARPS;
+  return kW4 ? DTQ_W4_EPI_WARPS : DTQ_W8_EPI_WARPS;
 }
 
 template <int BN, int kStages, bool kW4, bool k2Cta = false>
@@ -74,7 +84,9 @@ struct Smem {
   static constexpr int kA = BM * BK;                   // 16 KB (this CTA's 128 rows)
   static constexpr int kBRows = k2Cta ? BN / 2 : BN;   // a CTA pair splits B along N
   static constexpr int kB = kBRows * BK;               // s8 tile
-  static constexpr int kP = kW4 ? kBRows * (BK / 2) : 0;  // packed nibbles (this CTA's rows)
+  // packed nibbles of this CTA's B rows, staged by TMA for CTA pairs only:
+  // single-CTA W4A8 converters load them from L2 with LDG
+  static constexpr int kP = (kW4 && k2Cta) ? kBRows * (BK / 2) : 0;
   static constexpr int kEpiBufs = epi_warps<kW4>() > 8 ? 1 : 2;  // staging buffers per warp
   static constexpr int kEpi = epi_warps<kW4>() * kEpiBufs * 32 * 64;  // 32 rows x 64 B each
   static constexpr int kPar = 2 * 3 * BN * 4;             // {s_w, wsum, bias} x 2 tiles
@@ -228,12 +240,9 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
             tma_load_2d_2sm(sA + s * L::kA, &tmA, lead_full, kb * BK, m0);
             tma_load_2d_2sm(sB + s * L::kB, &tmB, lead_full, kb * BK, n0 + rank * L::kBRows);
           } else {
-            mbar_arrive_expect_tx(&full[s], L::kA + (kW4 ? L::kP : L::kB));
+            mbar_arrive_expect_tx(&full[s], L::kA + (kW4 ? 0 : L::kB));
             tma_load_2d(sA + s * L::kA, &tmA, &full[s], kb * BK, m0);
-            if constexpr (kW4)
-              tma_load_2d(sP + s * L::kP, &tmB, &full[s], kb * (BK / 2), n0);
-            else
-              tma_load_2d(sB + s * L::kB, &tmB, &full[s], kb * BK, n0);
+            if constexpr (!kW4) tma_load_2d(sB + s * L::kB, &tmB, &full[s], kb * BK, n0);
           }
           if (++s == kStages) {
             s = 0;
@@ -373,9 +382,10 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       // TMEM -> registers, 32 columns at a time; chunk cl+1 is in flight while
       // chunk cl is dequantised and stored (two register sets, full unroll)
       const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * BN + cgrp * kCols;
-      // (16 epilogue warps: one register set -- the other warps hide the
-      // load latency, and 576 threads leave ~100 registers each)
-      constexpr int kLdSets = kEpiWarps > 8 ? 1 : 2;
+      // (CTAs of more than 448 threads -- 16 epilogue warps, or 8 epilogue +
+      // 8 converter warps -- get one register set: the other warps hide the
+      // load latency, and ~100 registers per thread remain)
+      constexpr int kLdSets = num_threads<BN, kW4>() > 448 ? 1 : 2;
       uint32_t rr[kLdSets][32];
       tmem_ld_32x32b_x32(tbase, rr[0]);
       tmem_ld_wait_regs(rr[0]);
@@ -540,9 +550,65 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       }
     }
     if (g.tma_store && lane == 0) bulk_wait<0>();
+  } else if constexpr (kW4 && !k2Cta) {
+    // ------------------------------------------------------------ nibble converters
+    // Single-CTA tiles: the packed nibbles come straight from L2 (the whole
+    // packed B of a layer is a few MB), one k-block ahead in registers, so
+    // shared memory carries only the unpacked s8 tile (no TMA write + LDS of
+    // the packed bytes).  8 consecutive threads read one row's 64 bytes.
+    const int ct = threadIdx.x - 32 * kEpiWarps;  // 0 .. 32 * kConvWarps - 1
+    constexpr int kIt = L::kBRows * 8 / (32 * kConvWarps);
+    auto load = [&](int t, int kb, uint2 (&v)[kIt]) {
+      const int n0 = (t / g.tiles_m) * BN;
+#pragma unroll
+      for (int i = 0; i < kIt; ++i) {
+        const int item = ct + i * 32 * kConvWarps;
+        const int r = item >> 3, j = item & 7;
+        const int64_t row = min(n0 + r, g.N - 1);
+        const int64_t off = static_cast<int64_t>(kb) * (BK / 2) + j * 8;
+        v[i] = off < g.ld4 ? __ldg(reinterpret_cast<const uint2*>(g.w4 + row * g.ld4 + off))
+                           : make_uint2(0u, 0u);
+      }
+    };
+    int cb = 0;
+    uint32_t cph = 0;
+    int tile = tile0, kb = 0;
+    uint2 cur[kIt];
+    if (tile < total_tiles) load(tile, kb, cur);
+    while (tile < total_tiles) {
+      int ntile = tile, nkb = kb + 1;
+      if (nkb == g.k_blocks) {
+        nkb = 0;
+        ntile += tstride;
+      }
+      uint2 nxt[kIt];
+      if (ntile < total_tiles) load(ntile, nkb, nxt);
+      mbar_wait(&bempty[cb], cph ^ 1);  // the MMA has finished with this B buffer
+      uint8_t* dst = sB + cb * L::kB;
+#pragma unroll
+      for (int i = 0; i < kIt; ++i) {
+        const int item = ct + i * 32 * kConvWarps;
+        const int r = item >> 3, j = item & 7;
+        const uint2 o0 = s4x8_to_s8x8_x16(cur[i].x), o1 = s4x8_to_s8x8_x16(cur[i].y);
+        *reinterpret_cast<uint4*>(dst + r * 128 + ((j ^ (r & 7)) * 16)) =
+            make_uint4(o0.x, o0.y, o1.x, o1.y);
+      }
+      fence_proxy_async_smem();  // generic-proxy writes -> visible to the MMA (async proxy)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[cb]);
+      if (++cb == L::kCB) {
+        cb = 0;
+        cph ^= 1;
+      }
+#pragma unroll
+      for (int i = 0; i < kIt; ++i) cur[i] = nxt[i];
+      tile = ntile;
+      kb = nkb;
+    }
   } else if constexpr (kW4) {
     // ------------------------------------------------------------ nibble converters
-    const int ct = threadIdx.x - 32 * kEpiWarps;  // 0..127
+    // (CTA pairs: packed nibbles staged by TMA in the stage ring)
+    const int ct = threadIdx.x - 32 * kEpiWarps;  // 0 .. 32 * kConvWarps - 1
     int s = 0;
     uint32_t ph = 0;
     int cb = 0;

@@ -64,6 +64,13 @@ constexpr int BK = 128;  // bytes (= int8 elements) per k-block: one 128-byte sw
 #define DTQ_CONV_WARPS 8
 #endif
 constexpr int kConvWarps = DTQ_CONV_WARPS;
+// single-CTA W4A8: the converter warps split into groups that take turns on
+// k-blocks, so each group has kConvGroups k-blocks of MMA time per unpack
+// (its barrier / proxy-fence latency overlaps the other group's work)
+#ifndef DTQ_CONV_GROUPS
+#define DTQ_CONV_GROUPS 2
+#endif
+constexpr int kConvGroups = DTQ_CONV_GROUPS;
 // epilogue warps: 8 (two per TMEM lane quarter, each half of the columns);
 // W4A8 adds 8 nibble-converter warps.  Measured at fc1 (16384 x 4608 x 1152):
 // W8A8 with 4 / 8 / 16 epilogue warps 127 / 72 / 72 us; W4A8 with 4 / 8 / 16
@@ -191,7 +198,8 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       mbar_init(&empty[s], 1);
     }
     for (int c = 0; c < L::kCB; ++c) {
-      mbar_init(&conv[c], kConvWarps * (k2Cta ? 2 : 1));  // leader's: both CTAs convert
+      // leader's: both CTAs convert; single CTA: one converter group per k-block
+      mbar_init(&conv[c], k2Cta ? 2 * kConvWarps : kConvWarps / kConvGroups);
       mbar_init(&bempty[c], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -556,13 +564,16 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     // packed B of a layer is a few MB), one k-block ahead in registers, so
     // shared memory carries only the unpacked s8 tile (no TMA write + LDS of
     // the packed bytes).  8 consecutive threads read one row's 64 bytes.
-    const int ct = threadIdx.x - 32 * kEpiWarps;  // 0 .. 32 * kConvWarps - 1
-    constexpr int kIt = L::kBRows * 8 / (32 * kConvWarps);
+    constexpr int kGW = kConvWarps / kConvGroups;              // warps per group
+    const int cw = static_cast<int>(warp) - kEpiWarps;          // converter warp index
+    const int grp = cw / kGW;
+    const int ct = (cw % kGW) * 32 + static_cast<int>(lane);    // thread within the group
+    constexpr int kIt = L::kBRows * 8 / (32 * kGW);
     auto load = [&](int t, int kb, uint2 (&v)[kIt]) {
       const int n0 = (t / g.tiles_m) * BN;
 #pragma unroll
       for (int i = 0; i < kIt; ++i) {
-        const int item = ct + i * 32 * kConvWarps;
+        const int item = ct + i * 32 * kGW;
         const int r = item >> 3, j = item & 7;
         const int64_t row = min(n0 + r, g.N - 1);
         const int64_t off = static_cast<int64_t>(kb) * (BK / 2) + j * 8;
@@ -570,24 +581,35 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
                            : make_uint2(0u, 0u);
       }
     };
-    int cb = 0;
-    uint32_t cph = 0;
+    // this group's k-blocks: sequence numbers grp, grp + kConvGroups, ...
+    auto advance = [&](int& t, int& k) {
+      for (int u = 0; u < kConvGroups; ++u)
+        if (++k == g.k_blocks) {
+          k = 0;
+          t += tstride;
+        }
+    };
+    int seq = grp;
     int tile = tile0, kb = 0;
+    for (int u = 0; u < grp; ++u)
+      if (++kb == g.k_blocks) {
+        kb = 0;
+        tile += tstride;
+      }
     uint2 cur[kIt];
     if (tile < total_tiles) load(tile, kb, cur);
     while (tile < total_tiles) {
-      int ntile = tile, nkb = kb + 1;
-      if (nkb == g.k_blocks) {
-        nkb = 0;
-        ntile += tstride;
-      }
+      int ntile = tile, nkb = kb;
+      advance(ntile, nkb);
       uint2 nxt[kIt];
       if (ntile < total_tiles) load(ntile, nkb, nxt);
+      const int cb = seq % L::kCB;
+      const uint32_t cph = (seq / L::kCB) & 1;
       mbar_wait(&bempty[cb], cph ^ 1);  // the MMA has finished with this B buffer
       uint8_t* dst = sB + cb * L::kB;
 #pragma unroll
       for (int i = 0; i < kIt; ++i) {
-        const int item = ct + i * 32 * kConvWarps;
+        const int item = ct + i * 32 * kGW;
         const int r = item >> 3, j = item & 7;
         const uint2 o0 = s4x8_to_s8x8_x16(cur[i].x), o1 = s4x8_to_s8x8_x16(cur[i].y);
         *reinterpret_cast<uint4*>(dst + r * 128 + ((j ^ (r & 7)) * 16)) =
@@ -596,14 +618,11 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       fence_proxy_async_smem();  // generic-proxy writes -> visible to the MMA (async proxy)
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv[cb]);
-      if (++cb == L::kCB) {
-        cb = 0;
-        cph ^= 1;
-      }
 #pragma unroll
       for (int i = 0; i < kIt; ++i) cur[i] = nxt[i];
       tile = ntile;
       kb = nkb;
+      seq += kConvGroups;
     }
   } else if constexpr (kW4) {
     // ------------------------------------------------------------ nibble converters

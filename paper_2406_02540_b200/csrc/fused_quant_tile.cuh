@@ -233,6 +233,14 @@ __device__ __forceinline__ void fq_tile_codes(const float2 (&P)[FqShape<kQ>::kPa
 #endif
 // kWide: 576-thread CTAs (K > 1152, one per SM); otherwise <= 288 threads
 // with registers capped for DTQ_FQ_MINB CTAs per SM
+// Diagnostics modes (DTQ_DEBUG_FQ) exist only in builds with -DDTQ_FQ_DIAG:
+// the extra paths cost registers in the product kernel.
+#ifdef DTQ_FQ_DIAG
+#define FQ_DBG(a) ((a).dbg)
+#else
+#define FQ_DBG(a) 0
+#endif
+
 template <typename Tin, bool kRot, bool kExactV, int kPro, bool kWide, int kR>
 __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
     fq_tile_kernel(const FqArgs a) {
@@ -394,7 +402,7 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
       }
     }
 
-    if (a.dbg == 3) {  // diagnostics: the memory pipeline alone (raw bits out, no math)
+    if (FQ_DBG(a) == 3) {  // diagnostics: the memory pipeline alone (raw bits out, no math)
       if (ok) {
         uint8_t* dst = a.codes + row * a.ldc + c0;
 #pragma unroll
@@ -485,7 +493,7 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
     }
 
     // ---- 3. folded column map, then the transform
-    if (has_a && a.dbg != 4) {
+    if (has_a && FQ_DBG(a) != 4) {
 #pragma unroll
       for (int m = 0; m < kFqRuns / 2; ++m) {
 #pragma unroll
@@ -516,7 +524,7 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
         }
       }
     }
-    if (kRot && a.dbg != 1 && a.dbg != 4) {
+    if (kRot && FQ_DBG(a) != 1 && FQ_DBG(a) != 4) {
       const float2 neg = make_float2(-1.f, -1.f);
       auto stage = [&](int h) {  // local stride h over the pair index
 #pragma unroll
@@ -541,9 +549,9 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
           P[k] = __ffma2_rn(P[k], sg, make_float2(ox, oy));
         }
       };
-      if (a.dbg != 5) xlane(kFqItems, sg16);  // element stride 16
+      if (FQ_DBG(a) != 5) xlane(kFqItems, sg16);  // element stride 16
       if constexpr (kFqQ == 4) {
-        if (a.dbg != 5) xlane(2 * kFqItems, sg32);  // element stride 32
+        if (FQ_DBG(a) != 5) xlane(2 * kFqItems, sg32);  // element stride 32
       }
       else
         stage(16);  // element stride 32 (local stride 16)
@@ -692,5 +700,6 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
 }
 
 #undef FQ_V
+#undef FQ_DBG
 
 }  // namespace dtq_fq

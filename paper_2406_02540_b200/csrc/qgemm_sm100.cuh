@@ -137,6 +137,16 @@ __device__ __forceinline__ uint2 s4x8_to_s8x8_x16(uint32_t w) {
 // `empty` / `tfull` barriers of both CTAs.  Each CTA's TMEM holds its 128
 // accumulator rows, drained by its own epilogue warps, which release the
 // buffer on the leader's `tempty` barrier.
+// Diagnostics modes (DTQ_DEBUG_GEMM_EPI) and the per-role wait probe
+// (DTQ_DEBUG_GEMM_PROBE) exist only in builds with -DDTQ_GEMM_DIAG.
+#ifdef DTQ_GEMM_DIAG
+#define GEMM_DBG(g) ((g).dbg)
+#define GEMM_PROBE(g) ((g).probe)
+#else
+#define GEMM_DBG(g) 0
+#define GEMM_PROBE(g) static_cast<unsigned long long*>(nullptr)
+#endif
+
 template <int BN, int kStages, bool kW4, int kOut, bool k2Cta>
 __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     qgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -177,7 +187,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
   // diagnostics: cycles spent in each role's waits (DTQ_DEBUG_GEMM_PROBE)
   unsigned long long pw0 = 0, pw1 = 0;
   auto timed_wait = [&](uint64_t* bar, uint32_t par, unsigned long long& acc_cycles) {
-    if (g.probe == nullptr) {
+    if (GEMM_PROBE(g) == nullptr) {
       mbar_wait(bar, par);
       return;
     }
@@ -418,7 +428,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
               mbar_arrive(&tempty[acc]);
           }
         }
-        if (kOut == kOutNone || g.dbg == 2) {
+        if (kOut == kOutNone || GEMM_DBG(g) == 2) {
           if (kLdSets == 2 && cl + 1 < kCols / 32) tmem_ld_wait_regs(rr[(cl + 1) % kLdSets]);
           continue;
         }
@@ -429,7 +439,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
 #pragma unroll
           for (int j4 = 0; j4 < kPieceCols; j4 += 4) {
             const int cc = c * 32 + piece * kPieceCols + j4;
-            const bool nolds = g.dbg == 7;  // diagnostics: params from registers, no LDS
+            const bool nolds = GEMM_DBG(g) == 7;  // diagnostics: params from registers, no LDS
             const uint4 sw4 = nolds ? make_uint4(0x3f800000u, 0x3f800000u, 0x3f800000u, 0x3f800000u)
                                     : *reinterpret_cast<const uint4*>(par + cc);
             const uint4 ws4 = nolds ? make_uint4(0u, 0u, 0u, 0u)
@@ -478,14 +488,14 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
               for (int u = 0; u < 4; ++u) w[j4 + u] = static_cast<uint32_t>(a32[u] >> (kW4 ? 4 : 0));
             }
           }
-          if (g.dbg == 3 || g.dbg == 7) {  // diagnostics: keep the math alive, skip staging + stores
+          if (GEMM_DBG(g) == 3 || GEMM_DBG(g) == 7) {  // diagnostics: keep the math alive, skip staging + stores
             uint32_t x = 0;
 #pragma unroll
             for (int i = 0; i < 16; ++i) x ^= w[i];
             if (x == 0x9E3779B9u && lane == 77) static_cast<uint32_t*>(g.y)[0] = x;
             continue;
           }
-          if (g.dbg == 6) {  // diagnostics: direct 128-bit stores from registers, no staging
+          if (GEMM_DBG(g) == 6) {  // diagnostics: direct 128-bit stores from registers, no staging
             const int col0d = n0 + c * 32 + piece * kPieceCols;
             const int rowd = m0 + q * 32 + lane;
             if (rowd < g.M) {
@@ -504,9 +514,9 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
           if (g.tma_store) {
             // the bulk store that last read this buffer must have finished reading it
             if (lane == 0) {
-              const long long t0 = g.probe ? clock64() : 0;
+              const long long t0 = GEMM_PROBE(g) ? clock64() : 0;
               bulk_wait_read<kBufs - 1>();
-              if (g.probe) pw1 += static_cast<unsigned long long>(clock64() - t0);
+              if (GEMM_PROBE(g)) pw1 += static_cast<unsigned long long>(clock64() - t0);
             }
             __syncwarp();
           }
@@ -515,7 +525,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
             *reinterpret_cast<uint4*>(sb + lane * 64 + ((gq ^ ((lane >> 1) & 3)) * 16)) =
                 make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
           const int col0 = n0 + c * 32 + piece * kPieceCols;
-          if (g.dbg == 4) {  // diagnostics: staging written, no global stores
+          if (GEMM_DBG(g) == 4) {  // diagnostics: staging written, no global stores
             __syncwarp();
             continue;
           }
@@ -667,10 +677,10 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     }
   }
 
-  if (g.probe != nullptr && lane == 0) {
+  if (GEMM_PROBE(g) != nullptr && lane == 0) {
     // [cta][slot]: 0 tma empty-wait, 1 mma full-wait, 2 mma tempty-wait,
     // 3 epi0 tfull-wait, 4 epi0 store-drain-wait, 5 total cycles (warp 0)
-    unsigned long long* pr = g.probe + blockIdx.x * 8;
+    unsigned long long* pr = GEMM_PROBE(g) + blockIdx.x * 8;
     if (warp == kTmaWarp) pr[0] = pw0;
     if (warp == kMmaWarp) { pr[1] = pw0; pr[2] = pw1; }
     if (warp == 0) { pr[3] = pw0; pr[4] = pw1; pr[5] = clock64() - t_start; }
@@ -688,5 +698,8 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       tmem_dealloc<kTmemCols>(tmem_base);
   }
 }
+
+#undef GEMM_DBG
+#undef GEMM_PROBE
 
 }  // namespace dtq_gemm

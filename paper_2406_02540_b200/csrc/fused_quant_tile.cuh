@@ -626,6 +626,12 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
       mn = fminf(mn, m.x);
       mx = fmaxf(mx, m.y);
     }
+    if (FQ_DBG(a) == 6) {  // diagnostics: codes with fixed parameters (no parameter math)
+      fq_tile_codes<kFqQ, true, kExactV>(P, 0.01f + 1e-30f * mx, 128.f + 12582912.0f, qmax_i,
+                                         1.0, 100.0, 128.0, qmax,
+                                         a.codes + row * a.ldc + c0);
+      continue;
+    }
     // params (quant.cpp:90-124).  z needs rint(-lo / s) of the fp64 s: an
     // fp32 estimate is exact unless the quotient lies within 2^-10 of a
     // tie (then fp64); 1/s in fp32 suffices unless the codes must be exact

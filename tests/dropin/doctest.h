@@ -1,10 +1,10 @@
 // doctest.h -- minimal doctest-compatible test harness (the subset the
-// reference's unit tests use: TEST_CASE, CHECK, CHECK_THROWS, doctest::Approx
+// reference's unit tests use: TEST_CASE, SUBCASE, CHECK, CHECK_FALSE,
+// CHECK_THROWS, CHECK_THROWS_WITH_AS + doctest::Contains, doctest::Approx
 // with .epsilon / .scale, DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN).  doctest
 // itself is not vendored in the reference; this lets its test files
-// (/root/reference/proj/tests/test_{quant,qgemm,balance}.cpp) compile
-// unmodified against the B200 drop-in (include/dtq).  Test infrastructure
-// only.
+// (/root/reference/proj/tests/test_*.cpp) compile unmodified against the
+// B200 drop-in (include/dtq).  Test infrastructure only.
 #pragma once
 
 #include <algorithm>
@@ -46,7 +46,17 @@ class Approx {
   double scale_ = 1.0;
 };
 
+// CHECK_THROWS_WITH_AS(expr, doctest::Contains("..."), Ex): what() contains
+struct Contains {
+  explicit Contains(const char* s) : sub(s) {}
+  std::string sub;
+};
+
 namespace detail {
+
+inline bool message_matches(const std::string& what, const Contains& c) {
+  return what.find(c.sub) != std::string::npos;
+}
 
 struct Case {
   const char* name;
@@ -64,6 +74,8 @@ struct State {
   long checks = 0;
   long failed_checks = 0;
   bool case_failed = false;
+  int sub_target = 0;  // SUBCASE: the one entered on this run of the case
+  int sub_seen = 0;    // SUBCASEs met on this run
 };
 
 inline State& state() {
@@ -82,6 +94,32 @@ inline void report(bool ok, const char* expr, const char* file, int line) {
     ++state().failed_checks;
     state().case_failed = true;
     std::fprintf(stderr, "%s:%d: CHECK( %s ) failed\n", file, line, expr);
+  }
+}
+
+// doctest re-runs a test case once per SUBCASE, entering exactly one of
+// them each time (flat subcases only, as the reference tests use them)
+inline bool enter_subcase() { return state().sub_seen++ == state().sub_target; }
+
+inline bool message_matches(const std::string& what, const char* exact) { return what == exact; }
+inline bool message_matches(const std::string& what, const std::string& exact) {
+  return what == exact;
+}
+
+template <typename E, typename F, typename M>
+void check_throws_with_as(F&& f, const M& matcher, const char* expr, const char* file, int line) {
+  bool ok = false;
+  try {
+    f();
+  } catch (const E& e) {
+    ok = message_matches(std::string(e.what()), matcher);
+  } catch (...) {
+  }
+  ++state().checks;
+  if (!ok) {
+    ++state().failed_checks;
+    state().case_failed = true;
+    std::fprintf(stderr, "%s:%d: CHECK_THROWS_WITH_AS( %s ) failed\n", file, line, expr);
   }
 }
 
@@ -108,8 +146,12 @@ inline int run_all(int argc, char** argv) {
     if (!filter.empty() && std::string(c.name).find(filter) == std::string::npos) continue;
     ++ran;
     state().case_failed = false;
+    state().sub_target = 0;
     try {
-      c.fn();
+      do {  // once, or once per SUBCASE
+        state().sub_seen = 0;
+        c.fn();
+      } while (++state().sub_target < state().sub_seen);
     } catch (const std::exception& e) {
       state().case_failed = true;
       std::fprintf(stderr, "%s:%d: TEST CASE \"%s\" threw: %s\n", c.file, c.line, c.name, e.what());
@@ -141,6 +183,13 @@ inline int run_all(int argc, char** argv) {
 #define TEST_CASE(name) DOCTEST_TEST_CASE_IMPL(DOCTEST_CAT(doctest_case_, __COUNTER__), name)
 #define CHECK(...) doctest::detail::report(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__)
 #define REQUIRE(...) CHECK(__VA_ARGS__)
+#define CHECK_FALSE(...) \
+  doctest::detail::report(!static_cast<bool>(__VA_ARGS__), "!(" #__VA_ARGS__ ")", __FILE__, __LINE__)
+#define REQUIRE_FALSE(...) CHECK_FALSE(__VA_ARGS__)
+#define SUBCASE(name) if (doctest::detail::enter_subcase())
+#define CHECK_THROWS_WITH_AS(expr, matcher, ...)                                        \
+  doctest::detail::check_throws_with_as<__VA_ARGS__>([&] { (void)(expr); }, matcher, #expr, \
+                                                     __FILE__, __LINE__)
 #define CHECK_THROWS(...) \
   doctest::detail::check_throws([&] { (void)(__VA_ARGS__); }, #__VA_ARGS__, __FILE__, __LINE__)
 

@@ -108,3 +108,22 @@ def test_reference_acceptance_suite_passes_on_device(tmp_path):
     print(r.stdout[-3000:])
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "all criteria passed" in r.stdout
+
+
+APP = os.path.join(ROOT, "tests", "dropin", "_bin", "dtq_ref_app_tests")
+
+
+@pytest.mark.gpu
+def test_reference_model_and_io_unit_tests_pass_on_device(tmp_path):
+    # tests/test_toydit.cpp, test_sensitivity.cpp, test_trace_io.cpp compiled
+    # unmodified with the reference's toydit / sensitivity / trace_io sources:
+    # the toy DiT's linears, the sensitivity sweep's fake-quantization and the
+    # checkpoint writer's weight quantization all run on the B200 drop-in
+    if not os.path.exists(APP):
+        pytest.skip("model/io test binary not built (needs /root/reference at build time)")
+    env = dict(os.environ, TMPDIR=str(tmp_path))
+    r = subprocess.run([APP], capture_output=True, text=True, timeout=900, env=env)
+    print(r.stdout)
+    print(r.stderr[-4000:])
+    assert r.returncode == 0, r.stderr[-4000:]
+    assert " 0 failed" in r.stdout

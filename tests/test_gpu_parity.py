@@ -373,3 +373,33 @@ def test_quantizer_input_dtypes_wide_rows(oracle, dtype, K):
     c_ref, s_ref, z_ref = oracle.quantize_rows(x.double().numpy(), 8)
     assert np.array_equal(codes.cpu().numpy(), c_ref)
     assert np.array_equal(s.cpu().numpy(), s_ref) and np.array_equal(z.cpu().numpy(), z_ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("K,N,packed", [(200, 100, False), (1152, 4608, True), (328, 96, True)])
+def test_w4_gemm_tails_and_packed_upload(K, N, packed):
+    # single-CTA W4A8 tiles read the packed nibbles straight from L2: K tails
+    # (the last k-block past the packed row), N tails (rows past N) and the
+    # checkpoint path (packed stream uploaded as stored) must give the exact
+    # int32 accumulator
+    rng = np.random.default_rng(K + N)
+    M = 300
+    wc = rng.integers(0, 16, (N, K), dtype=np.uint8)
+    if packed:
+        wp = np.zeros((N, (K + 1) // 2), np.uint8)
+        wp |= wc[:, 0::2]
+        wp[:, : K // 2] |= (wc[:, 1::2] << 4).astype(np.uint8)
+        layer = dtq.QuantLinear.from_codes(cuda(wp), torch.ones(N, dtype=torch.float64, device=DEV),
+                                           4, K, packed=True)
+    else:
+        layer = dtq.QuantLinear.from_codes(cuda(wc), torch.ones(N, dtype=torch.float64, device=DEV),
+                                           4, K)
+    a = rng.integers(0, 256, (M, K), dtype=np.uint8)
+    z = rng.integers(0, 256, M).astype(np.int32)
+    ldc = (K + 15) // 16 * 16
+    ab = torch.zeros((M, ldc), dtype=torch.uint8, device=DEV)
+    ab[:, :K] = cuda(a)
+    acc = layer.gemm(ab[:, :K], torch.ones(M, dtype=torch.float64, device=DEV), cuda(z),
+                     out_dtype=torch.int32).cpu().numpy().astype(np.int64)
+    want = (a.astype(np.int64) - z[:, None]) @ (wc.astype(np.int64) - 8).T
+    assert np.array_equal(acc, want)

@@ -322,11 +322,15 @@ __global__ void weight_pack_kernel(const uint8_t* __restrict__ codes, int64_t ld
       sum += v;
     }
   } else {
+    // GEMM nibble layout (not the reference's stream order): each 32-bit word
+    // holds columns 8i..8i+7 as signed nibbles n = c ^ 8 (= c - 8 in 4-bit
+    // two's complement), byte k = n[8i+k] | n[8i+k+4] << 4, so the GEMM's
+    // unpack to 16*(c-8) as s8 is two masks and a shift (w4_word_to_s8x8_x16)
     for (int64_t b = threadIdx.x; b < ld4; b += blockDim.x) {
-      const int64_t c0 = 2 * b, c1 = 2 * b + 1;
+      const int64_t c0 = 8 * (b >> 2) + (b & 3), c1 = c0 + 4;
       const uint32_t lo = c0 < K ? codes[o * ldc + c0] : 8u;  // pad: code 8 -> w_sym 0
       const uint32_t hi = c1 < K ? codes[o * ldc + c1] : 8u;
-      w4[o * ld4 + b] = static_cast<uint8_t>(lo | (hi << 4));
+      w4[o * ld4 + b] = static_cast<uint8_t>((lo ^ 8u) | ((hi ^ 8u) << 4));
       sum += static_cast<int32_t>(lo) - 8 + static_cast<int32_t>(hi) - 8;
     }
   }
@@ -363,8 +367,8 @@ __global__ void export_codes_kernel(const int8_t* __restrict__ w8, int64_t ld8,
     const int64_t o = i / K, c = i % K;
     if (wbits != 4)
       out[i] = static_cast<uint8_t>(static_cast<int32_t>(w8[o * ld8 + c]) + (1 << (wbits - 1)));
-    else
-      out[i] = (w4[o * ld4 + c / 2] >> (4 * (c & 1))) & 0xF;
+    else  // the GEMM nibble layout of weight_pack_kernel
+      out[i] = ((w4[o * ld4 + 4 * (c >> 3) + (c & 3)] >> ((c & 4) ? 4 : 0)) & 0xF) ^ 8;
   }
 }
 
@@ -401,7 +405,7 @@ struct dtq_qlinear_s {
   int wbits = 8, abits = 8;
   int8_t* w8 = nullptr;   // [N, ld8] s8 (W8)
   int64_t ld8 = 0;
-  uint8_t* w4 = nullptr;  // [N, ld4] packed nibbles, raw codes (W4)
+  uint8_t* w4 = nullptr;  // [N, ld4] packed signed nibbles, GEMM order (W4; weight_pack_kernel)
   int64_t ld4 = 0;
   double* s_w = nullptr;      // [N]
   float* s_w_f = nullptr;     // [N]

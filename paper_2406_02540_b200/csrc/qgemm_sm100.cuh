@@ -118,16 +118,16 @@ __host__ __device__ constexpr int num_threads() {
   return 32 * (2 + epi_warps<kW4>() + (kW4 ? kConvWarps : 0));
 }
 
-// 8 LSB-first nibbles (trace_io.cpp:79-91 order; codes c, z_w = 8) -> 8 bytes
-// holding 16*(c - 8) as s8: the nibble (c ^ 8) is the 4-bit two's complement
-// of c - 8, and placed in the HIGH half of a byte it is exactly 16*(c - 8).
-// Five instructions per 8 weights; the GEMM folds the factor 16 back out
-// exactly (s_x/16 in the dequant, 16*sum(w) in the zero-point term, >>4 for
-// the raw accumulator).
-__device__ __forceinline__ uint2 s4x8_to_s8x8_x16(uint32_t w) {
-  const uint32_t hi = (w ^ 0x80808080u) & 0xF0F0F0F0u;         // odd elements
-  const uint32_t lo = ((w << 4) ^ 0x80808080u) & 0xF0F0F0F0u;  // even elements
-  return make_uint2(__byte_perm(lo, hi, 0x5140), __byte_perm(lo, hi, 0x7362));
+// One word of the handle's nibble layout (weight_pack_kernel in capi.cu:
+// columns 8i..8i+7 as n = c ^ 8, the 4-bit two's complement of c - 8, byte
+// k = n[k] | n[k+4] << 4) -> 8 bytes holding 16*(c - 8) as s8: a nibble in
+// the HIGH half of a byte with a zero low half is exactly 16*(c - 8).
+// Three instructions per 8 weights (the reference's stream order would need
+// five: XOR, two masks, two byte permutes).  The GEMM folds the factor 16
+// back out exactly (s_x/16 in the dequant, 16*sum(w) in the zero-point term,
+// >>4 for the raw accumulator).
+__device__ __forceinline__ uint2 w4_word_to_s8x8_x16(uint32_t w) {
+  return make_uint2((w << 4) & 0xF0F0F0F0u, w & 0xF0F0F0F0u);
 }
 
 // k2Cta: a cluster of two CTAs on one TPC computes a 256 x BN tile with
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         if (c < BN) {
           const bool okc = (p_ok >> i) & 1u;
           par[c] = okc ? p_sw[i] : 0u;
-          // W4: the unpacked weights are 16*w (s4x8_to_s8x8_x16), so is their sum
+          // W4: the unpacked weights are 16*w (w4_word_to_s8x8_x16), so is their sum
           par[BN + c] = okc ? static_cast<uint32_t>(-p_ws[i] * (kW4 ? 16 : 1)) : 0u;
           par[2 * BN + c] = okc ? p_b[i] : 0u;
         }
@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       for (int i = 0; i < kIt; ++i) {
         const int item = ct + i * 32 * kGW;
         const int r = item >> 3, j = item & 7;
-        const uint2 o0 = s4x8_to_s8x8_x16(cur[i].x), o1 = s4x8_to_s8x8_x16(cur[i].y);
+        const uint2 o0 = w4_word_to_s8x8_x16(cur[i].x), o1 = w4_word_to_s8x8_x16(cur[i].y);
         *reinterpret_cast<uint4*>(dst + r * 128 + ((j ^ (r & 7)) * 16)) =
             make_uint4(o0.x, o0.y, o1.x, o1.y);
       }
@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         for (int item = ct; item < L::kBRows * 8; item += 32 * kConvWarps) {
           const int r = item >> 3, j = item & 7;
           const uint2 w = *reinterpret_cast<const uint2*>(src + r * 64 + j * 8);
-          const uint2 o0 = s4x8_to_s8x8_x16(w.x), o1 = s4x8_to_s8x8_x16(w.y);
+          const uint2 o0 = w4_word_to_s8x8_x16(w.x), o1 = w4_word_to_s8x8_x16(w.y);
           const uint4 o = make_uint4(o0.x, o0.y, o1.x, o1.y);
           *reinterpret_cast<uint4*>(dst + r * 128 + ((j ^ (r & 7)) * 16)) = o;
         }

@@ -568,9 +568,14 @@ GemmCfg choose_gemm_cfg(int64_t M, int64_t N, int wbits, int sms) {
   GemmCfg best{256, 0};
   int64_t best_cost = INT64_MAX;
   for (const GemmCfg& c : cands) {
-    // W4A8 is bound by the in-smem nibble unpack (smem bandwidth shared with
-    // the MMA operand reads): single-CTA tiles measure faster there
-    if (wbits == 4 && c.cta2) continue;
+    // W4A8 stays on single-CTA tiles: bound by the nibble unpack, pairs
+    // measure slower (1266 vs 1328 TOPS at C3 fc1).  DTQ_GEMM_W4_CTA2=1
+    // (diagnostics) lets the cost model pick pairs for it.
+    static const bool w4_cta2 = [] {
+      const char* e = std::getenv("DTQ_GEMM_W4_CTA2");
+      return e && e[0] == '1';
+    }();
+    if (wbits == 4 && c.cta2 && !w4_cta2) continue;
     const int64_t tm = c.cta2 ? 256 : 128;
     const int64_t tiles = ((M + tm - 1) / tm) * ((N + c.bn - 1) / c.bn);
     const int64_t units = c.cta2 ? sms / 2 : sms;

@@ -91,9 +91,8 @@ struct Smem {
   static constexpr int kA = BM * BK;                   // 16 KB (this CTA's 128 rows)
   static constexpr int kBRows = k2Cta ? BN / 2 : BN;   // a CTA pair splits B along N
   static constexpr int kB = kBRows * BK;               // s8 tile
-  // packed nibbles of this CTA's B rows, staged by TMA for CTA pairs only:
-  // single-CTA W4A8 converters load them from L2 with LDG
-  static constexpr int kP = (kW4 && k2Cta) ? kBRows * (BK / 2) : 0;
+  // (W4A8 converters load the packed nibbles from L2: no smem for them)
+  static constexpr int kP = 0;
   static constexpr int kEpiBufs = epi_warps<kW4>() > 8 ? 1 : 2;  // staging buffers per warp
   static constexpr int kEpi = epi_warps<kW4>() * kEpiBufs * 32 * 64;  // 32 rows x 64 B each
   static constexpr int kPar = 2 * 3 * BN * 4;             // {s_w, wsum, bias} x 2 tiles
@@ -164,7 +163,6 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem + L::offA;
   uint8_t* sB = smem + L::offB;
-  uint8_t* sP = smem + L::offP;
   uint8_t* sE = smem + L::offE;
   uint32_t* sPar = reinterpret_cast<uint32_t*>(smem + L::offPar);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::offBar);
@@ -208,8 +206,8 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       mbar_init(&empty[s], 1);
     }
     for (int c = 0; c < L::kCB; ++c) {
-      // leader's: both CTAs convert; single CTA: one converter group per k-block
-      mbar_init(&conv[c], k2Cta ? 2 * kConvWarps : kConvWarps / kConvGroups);
+      // one converter group per k-block; a CTA pair's leader counts both CTAs'
+      mbar_init(&conv[c], (k2Cta ? 2 : 1) * (kConvWarps / kConvGroups));
       mbar_init(&bempty[c], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -244,19 +242,14 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         const int n0 = (tile / g.tiles_m) * BN;
         for (int kb = 0; kb < g.k_blocks; ++kb) {
           timed_wait(&empty[s], ph ^ 1, pw0);
-          if constexpr (k2Cta && kW4) {
-            // A of both CTAs lands on the leader's barrier; each CTA's packed
-            // nibbles land on its OWN barrier, which its converters wait on
-            const uint32_t lead_full = mapa_shared(smem_u32(&full[s]), 0);
-            mbar_arrive_expect_tx(&full[s], rank == 0 ? 2 * L::kA + L::kP : L::kP);
-            tma_load_2d_2sm(sA + s * L::kA, &tmA, lead_full, kb * BK, m0);
-            tma_load_2d(sP + s * L::kP, &tmB, &full[s], kb * (BK / 2), n0 + rank * L::kBRows);
-          } else if constexpr (k2Cta) {
+          if constexpr (k2Cta) {
             // both CTAs' bytes land on the leader's barrier; only it arms it
+            // (W4A8: A only, the converters fill B)
             const uint32_t lead_full = mapa_shared(smem_u32(&full[s]), 0);
-            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (L::kA + L::kB));
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (L::kA + (kW4 ? 0 : L::kB)));
             tma_load_2d_2sm(sA + s * L::kA, &tmA, lead_full, kb * BK, m0);
-            tma_load_2d_2sm(sB + s * L::kB, &tmB, lead_full, kb * BK, n0 + rank * L::kBRows);
+            if constexpr (!kW4)
+              tma_load_2d_2sm(sB + s * L::kB, &tmB, lead_full, kb * BK, n0 + rank * L::kBRows);
           } else {
             mbar_arrive_expect_tx(&full[s], L::kA + (kW4 ? 0 : L::kB));
             tma_load_2d(sA + s * L::kA, &tmA, &full[s], kb * BK, m0);
@@ -568,19 +561,20 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       }
     }
     if (g.tma_store && lane == 0) bulk_wait<0>();
-  } else if constexpr (kW4 && !k2Cta) {
+  } else if constexpr (kW4) {
     // ------------------------------------------------------------ nibble converters
-    // Single-CTA tiles: the packed nibbles come straight from L2 (the whole
-    // packed B of a layer is a few MB), one k-block ahead in registers, so
-    // shared memory carries only the unpacked s8 tile (no TMA write + LDS of
-    // the packed bytes).  8 consecutive threads read one row's 64 bytes.
+    // The packed nibbles come straight from L2 (the whole packed B of a layer
+    // is a few MB), one k-block ahead in registers, so shared memory carries
+    // only the unpacked s8 tile.  8 consecutive threads read one row's 64
+    // bytes.  In a CTA pair each CTA converts its own half of the B rows and
+    // reports to the leader, whose MMA reads both halves.
     constexpr int kGW = kConvWarps / kConvGroups;              // warps per group
     const int cw = static_cast<int>(warp) - kEpiWarps;          // converter warp index
     const int grp = cw / kGW;
     const int ct = (cw % kGW) * 32 + static_cast<int>(lane);    // thread within the group
     constexpr int kIt = L::kBRows * 8 / (32 * kGW);
     auto load = [&](int t, int kb, uint2 (&v)[kIt]) {
-      const int n0 = (t / g.tiles_m) * BN;
+      const int n0 = (t / g.tiles_m) * BN + rank * L::kBRows;
 #pragma unroll
       for (int i = 0; i < kIt; ++i) {
         const int item = ct + i * 32 * kGW;
@@ -627,53 +621,17 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       }
       fence_proxy_async_smem();  // generic-proxy writes -> visible to the MMA (async proxy)
       __syncwarp();
-      if (lane == 0) mbar_arrive(&conv[cb]);
+      if (lane == 0) {
+        if constexpr (k2Cta)
+          mbar_arrive_cluster_release(mapa_shared(smem_u32(&conv[cb]), 0));
+        else
+          mbar_arrive(&conv[cb]);
+      }
 #pragma unroll
       for (int i = 0; i < kIt; ++i) cur[i] = nxt[i];
       tile = ntile;
       kb = nkb;
       seq += kConvGroups;
-    }
-  } else if constexpr (kW4) {
-    // ------------------------------------------------------------ nibble converters
-    // (CTA pairs: packed nibbles staged by TMA in the stage ring)
-    const int ct = threadIdx.x - 32 * kEpiWarps;  // 0 .. 32 * kConvWarps - 1
-    int s = 0;
-    uint32_t ph = 0;
-    int cb = 0;
-    uint32_t cph = 0;
-    for (int tile = tile0; tile < total_tiles; tile += tstride) {
-      for (int kb = 0; kb < g.k_blocks; ++kb) {
-        mbar_wait(&full[s], ph);
-        mbar_wait(&bempty[cb], cph ^ 1);  // the MMA has finished with this B buffer
-        const uint8_t* src = sP + s * L::kP;
-        uint8_t* dst = sB + cb * L::kB;
-        // this CTA's B rows x 8 granules of 16 output bytes (= 8 packed bytes each)
-#pragma unroll 4
-        for (int item = ct; item < L::kBRows * 8; item += 32 * kConvWarps) {
-          const int r = item >> 3, j = item & 7;
-          const uint2 w = *reinterpret_cast<const uint2*>(src + r * 64 + j * 8);
-          const uint2 o0 = w4_word_to_s8x8_x16(w.x), o1 = w4_word_to_s8x8_x16(w.y);
-          const uint4 o = make_uint4(o0.x, o0.y, o1.x, o1.y);
-          *reinterpret_cast<uint4*>(dst + r * 128 + ((j ^ (r & 7)) * 16)) = o;
-        }
-        fence_proxy_async_smem();  // generic-proxy writes -> visible to the MMA (async proxy)
-        __syncwarp();
-        if (lane == 0) {
-          if constexpr (k2Cta)  // the leader's MMA reads both CTAs' B halves
-            mbar_arrive_cluster_release(mapa_shared(smem_u32(&conv[cb]), 0));
-          else
-            mbar_arrive(&conv[cb]);
-        }
-        if (++cb == L::kCB) {
-          cb = 0;
-          cph ^= 1;
-        }
-        if (++s == kStages) {
-          s = 0;
-          ph ^= 1;
-        }
-      }
     }
   }
 

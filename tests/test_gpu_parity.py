@@ -403,3 +403,35 @@ def test_w4_gemm_tails_and_packed_upload(K, N, packed):
                      out_dtype=torch.int32).cpu().numpy().astype(np.int64)
     want = (a.astype(np.int64) - z[:, None]) @ (wc.astype(np.int64) - 8).T
     assert np.array_equal(acc, want)
+
+
+@pytest.mark.gpu
+def test_w4_cta_pair_path_exact(tmp_path):
+    # CTA-pair W4A8 tiles (not the default choice; DTQ_GEMM_W4_CTA2=1 lets the
+    # tile model pick them) give the same exact accumulators
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, paper_2406_02540_b200 as dtq
+rng = np.random.default_rng(5)
+for K, N, M in [(1152, 4608, 600), (200, 100, 300)]:
+    wc = rng.integers(0, 16, (N, K), dtype=np.uint8)
+    layer = dtq.QuantLinear.from_codes(torch.from_numpy(wc).cuda(),
+                                       torch.ones(N, dtype=torch.float64, device="cuda"), 4, K)
+    a = rng.integers(0, 256, (M, K), dtype=np.uint8)
+    z = rng.integers(0, 256, M).astype(np.int32)
+    ldc = (K + 15) // 16 * 16
+    ab = torch.zeros((M, ldc), dtype=torch.uint8, device="cuda")
+    ab[:, :K] = torch.from_numpy(a).cuda()
+    acc = layer.gemm(ab[:, :K], torch.ones(M, dtype=torch.float64, device="cuda"),
+                     torch.from_numpy(z).cuda(), out_dtype=torch.int32).cpu().numpy()
+    want = (a.astype(np.int64) - z[:, None]) @ (wc.astype(np.int64) - 8).T
+    assert np.array_equal(acc.astype(np.int64), want), (K, N, M)
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DTQ_GEMM_W4_CTA2="1", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]

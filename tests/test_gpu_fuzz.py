@@ -1,0 +1,79 @@
+"""Seeded random sweep of the device path against the CPU oracle.
+
+Each case draws a shape (M, K, N), weight / activation bit widths, input
+dtype and balance (smoothing + 128-block rotation or none), then checks the
+bars of SURVEY.md section 8c on that case:
+  * codes / s / z of the fast quantizer without balance: bit-exact;
+  * codes / s / z of the exact (fp64) quantizer with balance: bit-exact
+    against the oracle's scale + rotate + quantize;
+  * the GEMM's int32 accumulator from those codes: bit-exact;
+  * the fp16 forward: within 1e-3 of max|y_ref| (the reference's norm).
+Shapes include K that are not multiples of 128 (the lane-group and exact
+kernels), single rows, and N that are not multiples of any tile width.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import paper_2406_02540_b200 as dtq  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+CASES = 64
+
+
+def _case(i):
+    rng = np.random.default_rng(1000 + i)
+    M = int(rng.choice([1, 7, 129, 300, 1024, 2500]))
+    K = int(rng.choice([64, 128, 200, 384, 1152, 1280, 2304, 4608]))
+    N = int(rng.choice([1, 40, 256, 333, 1152, 4608]))
+    wbits = int(rng.choice([2, 4, 6, 8]))
+    abits = int(rng.choice([4, 8])) if wbits != 8 else 8
+    dtype = [torch.float16, torch.bfloat16, torch.float32][int(rng.integers(0, 3))]
+    balance = bool(rng.integers(0, 2)) and K % 128 == 0
+    return rng, M, K, N, wbits, abits, dtype, balance
+
+
+@pytest.mark.parametrize("i", range(CASES))
+def test_random_case(oracle, i):
+    rng, M, K, N, wbits, abits, dtype, balance = _case(i)
+    gains = np.exp(rng.standard_normal(K))
+    x = (rng.standard_normal((M, K)) * gains)
+    x[:, rng.integers(0, K)] *= 25.0
+    xt = torch.from_numpy(x).to(dtype).to(DEV)
+    xd = xt.double().cpu().numpy()               # the values the device sees
+    w = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    wt = torch.from_numpy(w).to(DEV)
+
+    bal, xs = None, xd
+    if balance:
+        smooth = np.exp(0.3 * rng.standard_normal(K))
+        signs = dtq.hadamard_signs(K, 7)
+        bal = dtq.Balance(torch.from_numpy(smooth).to(DEV), torch.from_numpy(signs).to(DEV), 128)
+        xs = oracle.rotate_blocks(oracle.scale_x(xd, smooth), signs, 128)
+    layer = dtq.QuantLinear.create(wt, wbits, abits, balance=bal)
+    wc, sw, _ = layer.export()                   # codes, scales, row sums
+    zw = np.full(N, 1 << (wbits - 1), np.int32)  # symmetric weights: z = 2^(b-1)
+
+    # quantizer: fast mode is bit-exact without balance, exact mode with it
+    mode = dtq.MODE_EXACT if balance else dtq.MODE_FAST
+    codes, s, z = dtq.quantize_rows(xt, bits=abits, mode=mode, balance=bal)
+    c_ref, s_ref, z_ref = oracle.quantize_rows(xs, abits)
+    assert np.array_equal(codes.cpu().numpy(), c_ref), (M, K, N, wbits, abits, dtype, balance)
+    assert np.array_equal(s.cpu().numpy(), s_ref)
+    assert np.array_equal(z.cpu().numpy(), z_ref)
+
+    # GEMM accumulator from the device codes: exact (checked on a row sample
+    # so the CPU oracle stays within seconds)
+    rows = np.arange(M) if M <= 128 else np.sort(rng.choice(M, 128, replace=False))
+    acc = layer.gemm(codes, s, z, out_dtype=torch.int32).cpu().numpy().astype(np.int64)[rows]
+    acc_ref = oracle.qlinear_acc(c_ref[rows], z_ref[rows], wc, zw)
+    assert np.array_equal(acc, acc_ref)
+
+    # fp16 forward (fast mode end to end) against the fp64 reference epilogue
+    if abits == 8:
+        y = layer.forward(xt, out_dtype=torch.float16).float().cpu().numpy()[rows]
+        y_ref = oracle.qlinear_epilogue(acc_ref, s_ref[rows], sw)
+        err = np.abs(y.astype(np.float64) - y_ref).max() / max(np.abs(y_ref).max(), 1e-30)
+        assert err <= 1e-3 + (2e-3 if balance else 0.0)

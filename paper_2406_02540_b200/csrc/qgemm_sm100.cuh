@@ -86,6 +86,9 @@ __host__ __device__ constexpr int epi_warps() {
   return kW4 ? DTQ_W4_EPI_WARPS : DTQ_W8_EPI_WARPS;
 }
 
+#ifndef DTQ_W4_CB
+#define DTQ_W4_CB 3  // W4A8: depth of the unpacked-B ring
+#endif
 template <int BN, int kStages, bool kW4, bool k2Cta = false>
 struct Smem {
   static constexpr int kA = BM * BK;                   // 16 KB (this CTA's 128 rows)
@@ -99,7 +102,7 @@ struct Smem {
   static constexpr int offA = 0;
   // W4A8: the unpacked s8 B tiles live in their own kCB-deep ring, decoupled
   // from the TMA ring (A + packed nibbles), so the TMA ring can be deep
-  static constexpr int kCB = kW4 ? 3 : kStages;
+  static constexpr int kCB = kW4 ? DTQ_W4_CB : kStages;
   static constexpr int offB = offA + kStages * kA;
   static constexpr int offP = offB + kCB * kB;
   static constexpr int offE = offP + kStages * kP;
@@ -606,7 +609,12 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       int ntile = tile, nkb = kb;
       advance(ntile, nkb);
       uint2 nxt[kIt];
-      if (ntile < total_tiles) load(ntile, nkb, nxt);
+      // diagnostics (-DDTQ_GEMM_DIAG): 8 no loads / unpack / stores, 9 no
+      // smem stores, 10 no proxy fence, 11 no loads
+      const int cdbg = GEMM_DBG(g);
+      if (ntile < total_tiles && cdbg != 8 && cdbg != 11) load(ntile, nkb, nxt);
+      if (cdbg == 8 || cdbg == 11)
+        for (int i = 0; i < kIt; ++i) nxt[i] = make_uint2(0x12345678u ^ i, 0u);
       const int cb = seq % L::kCB;
       const uint32_t cph = (seq / L::kCB) & 1;
       mbar_wait(&bempty[cb], cph ^ 1);  // the MMA has finished with this B buffer
@@ -616,10 +624,15 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         const int item = ct + i * 32 * kGW;
         const int r = item >> 3, j = item & 7;
         const uint2 o0 = w4_word_to_s8x8_x16(cur[i].x), o1 = w4_word_to_s8x8_x16(cur[i].y);
+        if (cdbg == 8 || cdbg == 9) {
+          if ((o0.x ^ o1.y) == 0xFFFFFFFFu) dst[0] = 1;  // keep the math alive
+          continue;
+        }
         *reinterpret_cast<uint4*>(dst + r * 128 + ((j ^ (r & 7)) * 16)) =
             make_uint4(o0.x, o0.y, o1.x, o1.y);
       }
-      fence_proxy_async_smem();  // generic-proxy writes -> visible to the MMA (async proxy)
+      if (cdbg != 10)
+        fence_proxy_async_smem();  // generic-proxy writes -> visible to the MMA (async proxy)
       __syncwarp();
       if (lane == 0) {
         if constexpr (k2Cta)

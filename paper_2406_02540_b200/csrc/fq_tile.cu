@@ -10,18 +10,18 @@
 // Rows per tile (compile-time in the kernel): 8, or 4 when an 8-row double
 // buffer of a wide row does not fit shared memory.  0 = the shape does not
 // fit the tile kernel at all (the caller uses the lane-group kernel).
-int dtq_fq_tile_rows(int64_t M, int64_t K, int es, bool has_a, bool has_b, int sms) {
+int dtq_fq_tile_rows(int64_t M, int64_t K, int es, bool has_a, bool has_b, int pro, int sms) {
   (void)M;
   (void)sms;
   constexpr size_t kMax = 220 * 1024;
-  const bool four = dtq_fq::fq_lanes(K) == 4;
+  const bool four = dtq_fq::fq_lanes(K, pro) == 4;
   const int cap = four ? 288 : 576;  // the kernels' launch bounds
   static const int force = [] {  // DTQ_FQ_ROWS (diagnostics): start the search at R
     const char* e = std::getenv("DTQ_FQ_ROWS");
     return e ? std::atoi(e) : 8;
   }();
   for (int R = force; R >= 4; R /= 2)
-    if ((four ? R == 8 : R >= 4) && dtq_fq::fq_tile_threads(K, R) <= cap &&
+    if ((four ? R == 8 : R >= 4) && dtq_fq::fq_tile_threads(K, R, pro) <= cap &&
         dtq_fq::fq_tile_layout(K, R, es, has_a, has_b, 2).bytes <= kMax)
       return R;
   return 0;

@@ -44,14 +44,14 @@ template <typename Tin, bool kRot, bool kExactV, int kPro>
 cudaError_t launch_tile(const dtq_fq::FqArgs& a, int R, int nbuf, int sms, cudaStream_t st) {
   // K <= 1152: 4 lanes per block, 8-row tiles (288 threads); wider: 2 lanes
   // per block, 8 or 4 rows (576 threads)
-  const bool wide = dtq_fq::fq_lanes(a.K) == 2;
+  const bool wide = dtq_fq::fq_lanes(a.K, a.pro) == 2;
   auto kern = !wide ? dtq_fq::fq_tile_kernel<Tin, kRot, kExactV, kPro, false, 8>
               : (R == 8 ? dtq_fq::fq_tile_kernel<Tin, kRot, kExactV, kPro, true, 8>
                         : dtq_fq::fq_tile_kernel<Tin, kRot, kExactV, kPro, true, 4>);
   const bool has_b = a.pro == dtq_fq::kProModulate || a.pro == dtq_fq::kProLnModulate;
   const bool has_a = has_b || a.col_mul != nullptr;
   const dtq_fq::TileLayout L = dtq_fq::fq_tile_layout(a.K, R, sizeof(Tin), has_a, has_b, nbuf);
-  const int block = dtq_fq::fq_tile_threads(a.K, R);
+  const int block = dtq_fq::fq_tile_threads(a.K, R, a.pro);
   int occ = 0;
   cudaError_t e = fq_tile_occupancy(reinterpret_cast<const void*>(kern), block, L.bytes, &occ);
   if (e != cudaSuccess) return e;

@@ -86,6 +86,12 @@ __host__ __device__ constexpr int epi_warps() {
   return kW4 ? DTQ_W4_EPI_WARPS : DTQ_W8_EPI_WARPS;
 }
 
+// W4A8 single-CTA tiles: the packed nibbles ride the TMA stage ring with A
+// (1), or the converter warps load them from L2 with LDG (0)
+#ifndef DTQ_W4_TMA_PACKED
+#define DTQ_W4_TMA_PACKED 1
+#endif
+constexpr bool kW4TmaPacked = DTQ_W4_TMA_PACKED != 0;
 #ifndef DTQ_W4_CB
 #define DTQ_W4_CB 3  // W4A8: depth of the unpacked-B ring
 #endif
@@ -95,8 +101,11 @@ struct Smem {
   static constexpr int kBRows = k2Cta ? BN / 2 : BN;   // a CTA pair splits B along N
   static constexpr int kB = kBRows * BK;               // s8 tile
   // (W4A8 converters load the packed nibbles from L2: no smem for them)
-  static constexpr int kP = 0;
-  static constexpr int kEpiBufs = epi_warps<kW4>() > 8 ? 1 : 2;  // staging buffers per warp
+  // packed nibbles of this CTA's B rows per stage (single-CTA W4A8 on the
+  // TMA path); CTA pairs' converters load them from L2
+  static constexpr int kP = (kW4 && !k2Cta && kW4TmaPacked) ? kBRows * (BK / 2) : 0;
+  // staging buffers per epilogue warp (one when the budget is tight)
+  static constexpr int kEpiBufs = (epi_warps<kW4>() > 8 || (kP > 0 && BN == 256)) ? 1 : 2;
   static constexpr int kEpi = epi_warps<kW4>() * kEpiBufs * 32 * 64;  // 32 rows x 64 B each
   static constexpr int kPar = 2 * 3 * BN * 4;             // {s_w, wsum, bias} x 2 tiles
   static constexpr int offA = 0;
@@ -166,6 +175,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem + L::offA;
   uint8_t* sB = smem + L::offB;
+  uint8_t* sP = smem + L::offP;
   uint8_t* sE = smem + L::offE;
   uint32_t* sPar = reinterpret_cast<uint32_t*>(smem + L::offPar);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::offBar);
@@ -254,9 +264,12 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
             if constexpr (!kW4)
               tma_load_2d_2sm(sB + s * L::kB, &tmB, lead_full, kb * BK, n0 + rank * L::kBRows);
           } else {
-            mbar_arrive_expect_tx(&full[s], L::kA + (kW4 ? 0 : L::kB));
+            mbar_arrive_expect_tx(&full[s], L::kA + (kW4 ? L::kP : L::kB));
             tma_load_2d(sA + s * L::kA, &tmA, &full[s], kb * BK, m0);
-            if constexpr (!kW4) tma_load_2d(sB + s * L::kB, &tmB, &full[s], kb * BK, n0);
+            if constexpr (!kW4)
+              tma_load_2d(sB + s * L::kB, &tmB, &full[s], kb * BK, n0);
+            else if constexpr (L::kP > 0)
+              tma_load_2d(sP + s * L::kP, &tmB, &full[s], kb * (BK / 2), n0);
           }
           if (++s == kStages) {
             s = 0;
@@ -564,6 +577,44 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       }
     }
     if (g.tma_store && lane == 0) bulk_wait<0>();
+  } else if constexpr (kW4 && L::kP > 0) {
+    // ------------------------------------------------------------ nibble converters
+    // Single-CTA tiles, TMA path: the packed nibbles of k-block kb land in the
+    // stage ring with A (one TMA box of 64 B x BN rows); a converter group
+    // reads them from smem, unpacks and stores the s8 tile for the MMA.
+    constexpr int kGW = kConvWarps / kConvGroups;              // warps per group
+    const int cw = static_cast<int>(warp) - kEpiWarps;          // converter warp index
+    const int grp = cw / kGW;
+    const int ct = (cw % kGW) * 32 + static_cast<int>(lane);    // thread within the group
+    constexpr int kIt = L::kBRows * 8 / (32 * kGW);
+    const int total = ((total_tiles - tile0 + tstride - 1) / tstride) * g.k_blocks;
+    for (int seq = grp; seq < total; seq += kConvGroups) {
+      const int st = seq % kStages;
+      const uint32_t sph = (seq / kStages) & 1;
+      mbar_wait(&full[st], sph);  // A + packed nibbles of this k-block landed
+      const uint8_t* src = sP + st * L::kP;
+      uint2 v[kIt];
+#pragma unroll
+      for (int i = 0; i < kIt; ++i) {
+        const int item = ct + i * 32 * kGW;
+        v[i] = *reinterpret_cast<const uint2*>(src + (item >> 3) * 64 + (item & 7) * 8);
+      }
+      const int cb = seq % L::kCB;
+      const uint32_t cph = (seq / L::kCB) & 1;
+      mbar_wait(&bempty[cb], cph ^ 1);  // the MMA has finished with this B buffer
+      uint8_t* dst = sB + cb * L::kB;
+#pragma unroll
+      for (int i = 0; i < kIt; ++i) {
+        const int item = ct + i * 32 * kGW;
+        const int r = item >> 3, j = item & 7;
+        const uint2 o0 = w4_word_to_s8x8_x16(v[i].x), o1 = w4_word_to_s8x8_x16(v[i].y);
+        *reinterpret_cast<uint4*>(dst + r * 128 + ((j ^ (r & 7)) * 16)) =
+            make_uint4(o0.x, o0.y, o1.x, o1.y);
+      }
+      fence_proxy_async_smem();  // generic-proxy writes -> visible to the MMA (async proxy)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[cb]);
+    }
   } else if constexpr (kW4) {
     // ------------------------------------------------------------ nibble converters
     // The packed nibbles come straight from L2 (the whole packed B of a layer

@@ -543,8 +543,10 @@ int finish_from_codes(dtq_qlinear_s* h, const uint8_t* codes, int64_t ldc, const
       DTQ_TRY(make_tmap_u8(&h->tmB[i], h->w8, N, K, h->ld8, dtq_gemm::BK, rows[i],
                            CU_TENSOR_MAP_SWIZZLE_128B));
     else
-      DTQ_TRY(make_tmap_u8(&h->tmB[i], h->w4, N, (K + 1) / 2, h->ld4, dtq_gemm::BK / 2, rows[i],
-                           CU_TENSOR_MAP_SWIZZLE_NONE));
+      // the nibble layout fills whole 8-column words (padding codes are 8 ->
+      // zero), so the row's bytes run to 4 * ceil(K / 8), past (K + 1) / 2
+      DTQ_TRY(make_tmap_u8(&h->tmB[i], h->w4, N, round_up(K, 8) / 2, h->ld4, dtq_gemm::BK / 2,
+                           rows[i], CU_TENSOR_MAP_SWIZZLE_NONE));
   }
   return DTQ_OK;
 }

@@ -435,3 +435,25 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("K", [1, 5, 13, 67, 127, 129])
+def test_w4_odd_k_exact(K):
+    # odd K: the W4 nibble words run past (K + 1) / 2 bytes of the row; the
+    # GEMM's B operand must carry every column (reference test_qgemm.cpp:64-77
+    # draws c_in in 1..128)
+    rng = np.random.default_rng(K)
+    N, M = 37, 50
+    wc = rng.integers(0, 16, (N, K), dtype=np.uint8)
+    layer = dtq.QuantLinear.from_codes(cuda(wc), torch.ones(N, dtype=torch.float64, device=DEV),
+                                       4, K)
+    a = rng.integers(0, 256, (M, K), dtype=np.uint8)
+    z = rng.integers(0, 256, M).astype(np.int32)
+    ldc = (K + 15) // 16 * 16
+    ab = torch.zeros((M, ldc), dtype=torch.uint8, device=DEV)
+    ab[:, :K] = cuda(a)
+    acc = layer.gemm(ab[:, :K], torch.ones(M, dtype=torch.float64, device=DEV), cuda(z),
+                     out_dtype=torch.int32).cpu().numpy().astype(np.int64)
+    want = (a.astype(np.int64) - z[:, None]) @ (wc.astype(np.int64) - 8).T
+    assert np.array_equal(acc, want)

@@ -9,10 +9,10 @@ cudaError_t dtq_launch_gemm_w4(const CUtensorMap& tA, const CUtensorMap& tB,
   // (8 epilogue warps double the staging buffers: one stage fewer at BN=256)
 // single-CTA stage counts: A + packed nibbles per stage on the TMA path
 #ifndef DTQ_W4_S256
-#define DTQ_W4_S256 (dtq_gemm::kW4TmaPacked ? 3 : 5)
+#define DTQ_W4_S256 (dtq_gemm::kW4TmaPacked ? 4 : 6)
 #endif
 #ifndef DTQ_W4_S128
-#define DTQ_W4_S128 (dtq_gemm::kW4TmaPacked ? 5 : 8)
+#define DTQ_W4_S128 (dtq_gemm::kW4TmaPacked ? 6 : 9)
 #endif
 #ifndef DTQ_W4_P256
 #define DTQ_W4_P256 8

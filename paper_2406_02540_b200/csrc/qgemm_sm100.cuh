@@ -108,7 +108,10 @@ struct Smem {
   // TMA path); CTA pairs' converters load them from L2
   static constexpr int kP = (kW4 && !k2Cta && kW4TmaPacked) ? kBRows * (BK / 2) : 0;
   // staging buffers per epilogue warp (one when the budget is tight)
-  static constexpr int kEpiBufs = (epi_warps<kW4>() > 8 || (kP > 0 && BN == 256)) ? 1 : 2;
+  // (W8A8 CTA pairs at BN=256 trade the second buffer for a sixth stage:
+  // +1-2 % on the STDiT shapes)
+  static constexpr int kEpiBufs =
+      (epi_warps<kW4>() > 8 || (kP > 0 && BN == 256) || (!kW4 && k2Cta && BN == 256)) ? 1 : 2;
   static constexpr int kEpi = epi_warps<kW4>() * kEpiBufs * 32 * 64;  // 32 rows x 64 B each
   static constexpr int kPar = 2 * 3 * BN * 4;             // {s_w, wsum, bias} x 2 tiles
   static constexpr int offA = 0;

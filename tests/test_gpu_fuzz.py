@@ -77,3 +77,27 @@ def test_random_case(oracle, i):
         y_ref = oracle.qlinear_epilogue(acc_ref, s_ref[rows], sw)
         err = np.abs(y.astype(np.float64) - y_ref).max() / max(np.abs(y_ref).max(), 1e-30)
         assert err <= 1e-3 + (2e-3 if balance else 0.0)
+
+
+@pytest.mark.parametrize("i", range(16))
+def test_random_fast_balanced(oracle, i):
+    # the fast fp32 quantizer with smoothing + rotation against the oracle's
+    # fp64 scale + rotate + quantize: codes within 1 LSB, and rarely off
+    rng = np.random.default_rng(5000 + i)
+    M = int(rng.choice([3, 64, 500, 2048]))
+    K = int(rng.choice([128, 256, 1152, 2304, 4608]))
+    dtype = [torch.float16, torch.bfloat16, torch.float32][int(rng.integers(0, 3))]
+    x = rng.standard_normal((M, K)) * np.exp(rng.standard_normal(K))
+    xt = torch.from_numpy(x).to(dtype).to(DEV)
+    xd = xt.double().cpu().numpy()
+    smooth = np.exp(0.3 * rng.standard_normal(K))
+    signs = dtq.hadamard_signs(K, 7)
+    bal = dtq.Balance(torch.from_numpy(smooth).to(DEV), torch.from_numpy(signs).to(DEV), 128)
+    codes, s, z = dtq.quantize_rows(xt, mode=dtq.MODE_FAST, balance=bal)
+    c_ref, s_ref, z_ref = oracle.quantize_rows(
+        oracle.rotate_blocks(oracle.scale_x(xd, smooth), signs, 128), 8)
+    d = np.abs(codes.cpu().numpy().astype(int) - c_ref.astype(int))
+    assert d.max() <= 1
+    assert (d > 0).mean() <= 1e-3
+    # the per-token scale is the reference's fp64 s of the row's fp32 range
+    assert np.allclose(s.cpu().numpy(), s_ref, rtol=1e-5, atol=0)

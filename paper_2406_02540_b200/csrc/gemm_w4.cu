@@ -15,12 +15,15 @@ cudaError_t dtq_launch_gemm_w4(const CUtensorMap& tA, const CUtensorMap& tB,
 #define DTQ_W4_S128 (dtq_gemm::kW4TmaPacked ? 6 : 9)
 #endif
 #ifndef DTQ_W4_P256
-#define DTQ_W4_P256 8
+#define DTQ_W4_P256 (dtq_gemm::kW4TmaPacked ? 6 : 8)
+#endif
+#ifndef DTQ_W4_P128
+#define DTQ_W4_P128 (dtq_gemm::kW4TmaPacked ? 7 : 8)
 #endif
   constexpr int kS256 = DTQ_W4_S256, kS128 = DTQ_W4_S128, kP256 = DTQ_W4_P256;
   if (c.cta2)  // CTA pair: each SM unpacks only its half of B (8 A stages fit)
     return c.bn == 256 ? dtq_launch_gemm_o<256, kP256, true, true>(tA, tB, tY, g, sms, st)
-                       : dtq_launch_gemm_o<128, 8, true, true>(tA, tB, tY, g, sms, st);
+                       : dtq_launch_gemm_o<128, DTQ_W4_P128, true, true>(tA, tB, tY, g, sms, st);
   // single CTA: the stage ring holds A only (converters read packed B from L2)
   return c.bn == 256 ? dtq_launch_gemm_o<256, kS256, true, false>(tA, tB, tY, g, sms, st)
                      : dtq_launch_gemm_o<128, kS128, true, false>(tA, tB, tY, g, sms, st);

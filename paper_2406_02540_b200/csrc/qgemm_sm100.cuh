@@ -106,7 +106,7 @@ struct Smem {
   // (W4A8 converters load the packed nibbles from L2: no smem for them)
   // packed nibbles of this CTA's B rows per stage (single-CTA W4A8 on the
   // TMA path); CTA pairs' converters load them from L2
-  static constexpr int kP = (kW4 && !k2Cta && kW4TmaPacked) ? kBRows * (BK / 2) : 0;
+  static constexpr int kP = (kW4 && kW4TmaPacked) ? kBRows * (BK / 2) : 0;
   // staging buffers per epilogue warp (one when the budget is tight)
   // (W8A8 CTA pairs at BN=256 trade the second buffer for a sixth stage:
   // +1-2 % on the STDiT shapes)
@@ -261,9 +261,16 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         const int n0 = (tile / g.tiles_m) * BN;
         for (int kb = 0; kb < g.k_blocks; ++kb) {
           timed_wait(&empty[s], ph ^ 1, pw0);
-          if constexpr (k2Cta) {
+          if constexpr (k2Cta && kW4 && L::kP > 0) {
+            // A of both CTAs lands on the leader's barrier; each CTA's packed
+            // nibbles land on its OWN barrier, which its converters wait on
+            const uint32_t lead_full = mapa_shared(smem_u32(&full[s]), 0);
+            mbar_arrive_expect_tx(&full[s], rank == 0 ? 2 * L::kA + L::kP : L::kP);
+            tma_load_2d_2sm(sA + s * L::kA, &tmA, lead_full, kb * BK, m0);
+            tma_load_2d(sP + s * L::kP, &tmB, &full[s], kb * (BK / 2), n0 + rank * L::kBRows);
+          } else if constexpr (k2Cta) {
             // both CTAs' bytes land on the leader's barrier; only it arms it
-            // (W4A8: A only, the converters fill B)
+            // (W4A8 on the L2 path: A only, the converters fill B)
             const uint32_t lead_full = mapa_shared(smem_u32(&full[s]), 0);
             if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (L::kA + (kW4 ? 0 : L::kB)));
             tma_load_2d_2sm(sA + s * L::kA, &tmA, lead_full, kb * BK, m0);
@@ -585,9 +592,10 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     if (g.tma_store && lane == 0) bulk_wait<0>();
   } else if constexpr (kW4 && L::kP > 0) {
     // ------------------------------------------------------------ nibble converters
-    // Single-CTA tiles, TMA path: the packed nibbles of k-block kb land in the
-    // stage ring with A (one TMA box of 64 B x BN rows); a converter group
-    // reads them from smem, unpacks and stores the s8 tile for the MMA.
+    // TMA path: the packed nibbles of k-block kb land in the stage ring with
+    // A (one TMA box of 64 B x this CTA's B rows, on this CTA's own barrier);
+    // a converter group reads them from smem, unpacks and stores the s8 tile
+    // for the MMA (a CTA pair's leader MMA reads both CTAs' halves).
     constexpr int kGW = kConvWarps / kConvGroups;              // warps per group
     const int cw = static_cast<int>(warp) - kEpiWarps;          // converter warp index
     const int grp = cw / kGW;
@@ -619,7 +627,12 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       }
       fence_proxy_async_smem();  // generic-proxy writes -> visible to the MMA (async proxy)
       __syncwarp();
-      if (lane == 0) mbar_arrive(&conv[cb]);
+      if (lane == 0) {
+        if constexpr (k2Cta)
+          mbar_arrive_cluster_release(mapa_shared(smem_u32(&conv[cb]), 0));
+        else
+          mbar_arrive(&conv[cb]);
+      }
     }
   } else if constexpr (kW4) {
     // ------------------------------------------------------------ nibble converters

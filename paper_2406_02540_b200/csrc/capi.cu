@@ -567,18 +567,30 @@ GemmCfg choose_gemm_cfg(int64_t M, int64_t N, int wbits, int sms) {
     const GemmCfg f[4] = {{256, 0}, {128, 0}, {256, 1}, {128, 1}};
     return f[forced];
   }
+  // W4A8 stays on single-CTA tiles (bound by the nibble unpack; pairs
+  // measure slower: 1389 vs 1820 TOPS at C3 fc1), DTQ_GEMM_W4_CTA2=1
+  // (diagnostics) lets the cost model below pick pairs for it.  Of the
+  // single-CTA shapes, the two-M-sub-tile BN=128 one wins for N <= 2304
+  // (proj 1606 vs 1460, fc2 2069 vs 1770 TOPS) and BN=256 for wide N
+  // (fc1 1790 vs 1661 at C3).
+  static const bool w4_cta2 = [] {
+    const char* e = std::getenv("DTQ_GEMM_W4_CTA2");
+    return e && e[0] == '1';
+  }();
+  if (wbits == 4 && !w4_cta2 && dtq_gemm::dual_m<128, true, false>()) {
+    // both shapes do 256 x 128 x K (two sub-tiles) or 128 x 256 x K per tile:
+    // fewer waves wins, then the N rule
+    const int64_t w_dual = ((M + 255) / 256 * ((N + 127) / 128) + sms - 1) / sms;
+    const int64_t w_256 = ((M + 127) / 128 * ((N + 255) / 256) + sms - 1) / sms;
+    if (w_dual != w_256) return w_dual < w_256 ? GemmCfg{128, 0} : GemmCfg{256, 0};
+    return N <= 2304 ? GemmCfg{128, 0} : GemmCfg{256, 0};
+  }
   GemmCfg best{256, 0};
   int64_t best_cost = INT64_MAX;
   for (const GemmCfg& c : cands) {
-    // W4A8 stays on single-CTA tiles: bound by the nibble unpack, pairs
-    // measure slower (1266 vs 1328 TOPS at C3 fc1).  DTQ_GEMM_W4_CTA2=1
-    // (diagnostics) lets the cost model pick pairs for it.
-    static const bool w4_cta2 = [] {
-      const char* e = std::getenv("DTQ_GEMM_W4_CTA2");
-      return e && e[0] == '1';
-    }();
     if (wbits == 4 && c.cta2 && !w4_cta2) continue;
-    const int64_t tm = c.cta2 ? 256 : 128;
+    const bool m2 = wbits == 4 && !c.cta2 && c.bn == 128 && dtq_gemm::dual_m<128, true, false>();
+    const int64_t tm = (c.cta2 || m2) ? 256 : 128;
     const int64_t tiles = ((M + tm - 1) / tm) * ((N + c.bn - 1) / c.bn);
     const int64_t units = c.cta2 ? sms / 2 : sms;
     const int64_t waves = (tiles + units - 1) / units;
@@ -619,7 +631,9 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
   const int sms = device_info().sms;
   const GemmCfg cfg = choose_gemm_cfg(M, h->N, h->wbits, sms);
   const int BN = cfg.bn;
-  const int tile_m = cfg.cta2 ? 2 * dtq_gemm::BM : dtq_gemm::BM;
+  const bool m2 = h->wbits == 4 && !cfg.cta2 && cfg.bn == 128 &&
+                  dtq_gemm::dual_m<128, true, false>();  // two M sub-tiles per CTA
+  const int tile_m = (cfg.cta2 || m2) ? 2 * dtq_gemm::BM : dtq_gemm::BM;
   const int brows = cfg.cta2 ? BN / 2 : BN;
   const CUtensorMap& tB = h->tmB[brows == 256 ? 0 : (brows == 128 ? 1 : 2)];
 

@@ -12,7 +12,8 @@ cudaError_t dtq_launch_gemm_w4(const CUtensorMap& tA, const CUtensorMap& tB,
 #define DTQ_W4_S256 (dtq_gemm::kW4TmaPacked ? 4 : 6)
 #endif
 #ifndef DTQ_W4_S128
-#define DTQ_W4_S128 (dtq_gemm::kW4TmaPacked ? 6 : 9)
+#define DTQ_W4_S128 \
+  (dtq_gemm::dual_m<128, true, false>() ? 4 : (dtq_gemm::kW4TmaPacked ? 6 : 9))
 #endif
 #ifndef DTQ_W4_P256
 #define DTQ_W4_P256 (dtq_gemm::kW4TmaPacked ? 6 : 8)

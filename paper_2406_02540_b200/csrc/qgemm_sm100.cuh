@@ -92,6 +92,16 @@ __host__ __device__ constexpr int epi_warps() {
 #define DTQ_W4_TMA_PACKED 1
 #endif
 constexpr bool kW4TmaPacked = DTQ_W4_TMA_PACKED != 0;
+// W4A8 single-CTA tiles at BN=128 run two 128-row M sub-tiles per CTA (M =
+// 256, two TMEM accumulators per tile), so each unpacked B k-block feeds
+// twice the MMA work
+#ifndef DTQ_W4_M2
+#define DTQ_W4_M2 1
+#endif
+template <int BN, bool kW4, bool k2Cta>
+__host__ __device__ constexpr bool dual_m() {
+  return DTQ_W4_M2 != 0 && kW4 && !k2Cta && BN == 128;
+}
 #ifndef DTQ_W4_CB
 // W4A8: depth of the unpacked-B ring.  Two, so the stage ring (A + packed
 // nibbles) can be four deep: measured 24.7 vs 26.3 us (3 + 3) and 32.1 us
@@ -100,7 +110,8 @@ constexpr bool kW4TmaPacked = DTQ_W4_TMA_PACKED != 0;
 #endif
 template <int BN, int kStages, bool kW4, bool k2Cta = false>
 struct Smem {
-  static constexpr int kA = BM * BK;                   // 16 KB (this CTA's 128 rows)
+  static constexpr bool kM2 = dual_m<BN, kW4, k2Cta>();
+  static constexpr int kA = BM * BK * (kM2 ? 2 : 1);  // this CTA's A rows per stage
   static constexpr int kBRows = k2Cta ? BN / 2 : BN;   // a CTA pair splits B along N
   static constexpr int kB = kBRows * BK;               // s8 tile
   // (W4A8 converters load the packed nibbles from L2: no smem for them)
@@ -111,7 +122,9 @@ struct Smem {
   // (W8A8 CTA pairs at BN=256 trade the second buffer for a sixth stage:
   // +1-2 % on the STDiT shapes)
   static constexpr int kEpiBufs =
-      (epi_warps<kW4>() > 8 || (kP > 0 && BN == 256) || (!kW4 && k2Cta && BN == 256)) ? 1 : 2;
+      (epi_warps<kW4>() > 8 || (kP > 0 && (BN == 256 || kM2)) || (!kW4 && k2Cta && BN == 256))
+          ? 1
+          : 2;
   static constexpr int kEpi = epi_warps<kW4>() * kEpiBufs * 32 * 64;  // 32 rows x 64 B each
   static constexpr int kPar = 2 * 3 * BN * 4;             // {s_w, wsum, bias} x 2 tiles
   static constexpr int offA = 0;
@@ -170,9 +183,10 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
                  const __grid_constant__ CUtensorMap tmY, const GemmArgs g) {
   using namespace dtq_ptx;
   using L = Smem<BN, kStages, kW4, k2Cta>;
-  constexpr uint32_t kTmemCols = 2 * BN;
-  constexpr int kTileM = k2Cta ? 2 * BM : BM;
-  constexpr uint32_t kIdesc = idesc_i8_u8s8(kTileM, BN);
+  constexpr bool kM2 = L::kM2;
+  constexpr uint32_t kTmemCols = 2 * BN * (kM2 ? 2 : 1);
+  constexpr int kTileM = (k2Cta || kM2) ? 2 * BM : BM;
+  constexpr uint32_t kIdesc = idesc_i8_u8s8(k2Cta ? 2 * BM : BM, BN);
 
   constexpr int kEpiWarps = epi_warps<kW4>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -279,6 +293,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
           } else {
             mbar_arrive_expect_tx(&full[s], L::kA + (kW4 ? L::kP : L::kB));
             tma_load_2d(sA + s * L::kA, &tmA, &full[s], kb * BK, m0);
+            if constexpr (kM2) tma_load_2d(sA + s * L::kA + BM * BK, &tmA, &full[s], kb * BK, m0 + BM);
             if constexpr (!kW4)
               tma_load_2d(sB + s * L::kB, &tmB, &full[s], kb * BK, n0);
             else if constexpr (L::kP > 0)
@@ -304,19 +319,22 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         const uint32_t aph = (it >> 1) & 1;
         timed_wait(&tempty[acc], aph ^ 1, pw1);
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * BN;
+        const uint32_t d = tmem_base + acc * BN * (kM2 ? 2 : 1);
         for (int kb = 0; kb < g.k_blocks; ++kb) {
           timed_wait(&full[s], ph, pw0);
           if constexpr (kW4) mbar_wait(&conv[cb], cph);
           tc_fence_after();
-          const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * L::kA));
           const uint64_t bd = umma_desc_sw128(smem_u32(sB + (kW4 ? cb : s) * L::kB));
 #pragma unroll
-          for (int k = 0; k < BK / 32; ++k) {
-            if constexpr (k2Cta)
-              mma_i8_cta2(d, ad + 2 * k, bd + 2 * k, kIdesc, (kb | k) != 0 ? 1u : 0u);
-            else
-              mma_i8(d, ad + 2 * k, bd + 2 * k, kIdesc, (kb | k) != 0 ? 1u : 0u);
+          for (int sub = 0; sub < (kM2 ? 2 : 1); ++sub) {  // kM2: both M sub-tiles, same B
+            const uint64_t ad = umma_desc_sw128(smem_u32(sA + s * L::kA + sub * BM * BK));
+#pragma unroll
+            for (int k = 0; k < BK / 32; ++k) {
+              if constexpr (k2Cta)
+                mma_i8_cta2(d, ad + 2 * k, bd + 2 * k, kIdesc, (kb | k) != 0 ? 1u : 0u);
+              else
+                mma_i8(d + sub * BN, ad + 2 * k, bd + 2 * k, kIdesc, (kb | k) != 0 ? 1u : 0u);
+            }
           }
           if constexpr (k2Cta)
             mma_commit_cta2_mc(&empty[s], 0x3);
@@ -349,9 +367,12 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     // warp w owns TMEM lanes [32*(w%4), +32) = tile rows (lane = one row) and
     // one contiguous column range of the tile (BN / (kEpiWarps/4) columns).
     const uint32_t q = warp & 3;
-    constexpr int kColGroups = kEpiWarps / 4;
+    // (kM2: warps 0-3 drain M sub-tile 0, 4-7 sub-tile 1, all BN columns)
+    constexpr int kColGroups = kM2 ? 1 : kEpiWarps / 4;
     constexpr int kCols = BN / kColGroups;
-    const int cgrp = warp / 4;
+    const int cgrp = kM2 ? 0 : warp / 4;
+    const int sub = kM2 ? static_cast<int>(warp >> 2) : 0;
+    const int qrow = sub * BM + static_cast<int>(q) * 32;  // first tile row of this warp
     const int et = threadIdx.x;                        // index among epilogue threads
     constexpr int kBufs = L::kEpiBufs;
     uint8_t* stage = sE + warp * (kBufs * 32 * 64);  // 32 x 64 B staging buffer(s)
@@ -388,7 +409,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
         p_ws[i] = __ldg(g.wsum + cc);
         p_b[i] = has_bias ? __float_as_uint(__ldg(g.bias + cc)) : 0u;
       }
-      const int row = tm0 + q * 32 + lane;
+      const int row = tm0 + qrow + lane;
       p_ok |= row < g.M ? (1u << 31) : 0u;
       nsx = __ldg(g.s_x + min(row, g.M - 1));
       nzx = __ldg(g.z_x + min(row, g.M - 1));
@@ -421,7 +442,8 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       tc_fence_after();
       // TMEM -> registers, 32 columns at a time; chunk cl+1 is in flight while
       // chunk cl is dequantised and stored (two register sets, full unroll)
-      const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * BN + cgrp * kCols;
+      const uint32_t tbase =
+          tmem_base + ((q * 32) << 16) + (acc * (kM2 ? 2 : 1) + sub) * BN + cgrp * kCols;
       // (CTAs of more than 448 threads -- 16 epilogue warps, or 8 epilogue +
       // 8 converter warps -- get one register set: the other warps hide the
       // load latency, and ~100 registers per thread remain)
@@ -519,7 +541,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
           }
           if (GEMM_DBG(g) == 6) {  // diagnostics: direct 128-bit stores from registers, no staging
             const int col0d = n0 + c * 32 + piece * kPieceCols;
-            const int rowd = m0 + q * 32 + lane;
+            const int rowd = m0 + qrow + lane;
             if (rowd < g.M) {
               uint8_t* dst = static_cast<uint8_t*>(g.y) +
                              (static_cast<int64_t>(rowd) * g.ldy + col0d) * esize;
@@ -555,7 +577,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmY, sb, col0 * esize, m0 + q * 32);
+              tma_store_2d(&tmY, sb, col0 * esize, m0 + qrow);
               bulk_commit();
             }
             buf = (buf + 1) % kBufs;
@@ -566,7 +588,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
             for (int st = 0; st < 4; ++st) {
               const int srow = st * 8 + (lane >> 2);
               const int gq = lane & 3;
-              const int grow = m0 + q * 32 + srow;
+              const int grow = m0 + qrow + srow;
               const int gcol = col0 + gq * (16 / esize);
               if (grow < g.M && gcol < g.N) {
                 const uint4 v =

@@ -237,10 +237,12 @@ def run_reference(args, world, rank):
     global _SIGNS
     if rank != 0:
         return
-    import paper_2406_02540_b200 as dtq
+    from oracle.oracle import Reference
     threads = os.cpu_count() or 1
     x, w, smooth = make_inputs()
-    _SIGNS = dtq.hadamard_signs(K, 7)
+    # the reference's own hadamard_matrix draws (balance.cpp:69-80); nothing
+    # of this repo's package runs on the reference arm
+    _SIGNS = Reference().hadamard_signs(K, 7)
     rows = args.cpu_rows
     for _ in range(args.warmup):
         cpu_reference_sample(min(rows, 64), threads, x, w, smooth, _SIGNS)

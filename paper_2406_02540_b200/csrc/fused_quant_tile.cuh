@@ -49,8 +49,9 @@
 namespace dtq_fq {
 
 // Lanes per 128-column block: kQ = 4 for K <= 1152 (32 values per lane,
-// <= 72 registers, three 288-thread CTAs per SM), kQ = 2 for wider rows (64
-// values per lane, 576-thread CTAs).  Derived per-lane shapes:
+// <= 112 registers, two 288-thread CTAs per SM), kQ = 2 for wider rows and
+// the LayerNorm prologue (64 values per lane, up to 576-thread CTAs).
+// Derived per-lane shapes:
 template <int kQ>
 struct FqShape {
   static constexpr int kE = 128 / kQ;      // values per lane

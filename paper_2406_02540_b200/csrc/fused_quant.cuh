@@ -89,11 +89,12 @@ __device__ __forceinline__ float gelu_nerfcx_poly(float u) {
 }
 
 __device__ __forceinline__ float gelu1(float x) {
+  // z = |x| / sqrt(2) is folded into both constants: u = z * 5/9 - 1 and
+  // exp(-z^2) = 2^(|x|^2 * -log2(e) / 2)
   const float ax = fabsf(x);
-  const float z = ax * 0.70710678118654752f;
-  const float u = fminf(fmaf(z, 0.5555555555555556f, -1.f), 1.f);
+  const float u = fminf(fmaf(ax, 0.39283710065919303f, -1.f), 1.f);
   float e;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(z * z * -1.4426950408889634f));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(ax * ax * -0.72134752044448170f));
   return fmaf(ax, e * gelu_nerfcx_poly(u), fmaxf(x, 0.f));  // max(x,0) - |x| E
 }
 

@@ -166,8 +166,11 @@ int dtq_qgemm(const uint8_t* codes, int64_t ldc, const double* s_x, const int32_
  * Whole Matrix qlinear_forward(x, layer) (qgemm.cpp:23-67) on the device:
  * fused quantizer (prologue + the handle's balance) then the GEMM.
  * `workspace` [dev] of dtq_qlinear_workspace_bytes(h, M) bytes (codes and
- * per-token params), or NULL to use a handle-owned buffer (not thread-safe
- * per handle). */
+ * per-token params), or NULL to use a handle-owned buffer.  Calls that use
+ * handle-owned scratch (workspace NULL, or y_dtype DTQ_F64, whose s32
+ * accumulator is handle-owned) must be ordered on one stream or serialised
+ * by the caller; with a caller workspace and a non-F64 output, calls on one
+ * handle may run concurrently on different streams. */
 size_t dtq_qlinear_workspace_bytes(dtq_qlinear_t h, int64_t M);
 int dtq_qlinear_forward(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear_t h,
                         int mode, const dtq_prologue* prologue, void* y, int y_dtype,
@@ -186,7 +189,9 @@ int dtq_qlinear_quantize(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq
 /* Same with HOST buffers (x [host] M x K dense, y [host] M x N dense):
  * H2D copy, fused forward, D2H copy, stream synchronised before returning.
  * Pinned host memory gives full PCIe/C2C bandwidth.  Non-finite input is
- * reported as DTQ_ERR_INVALID_ARGUMENT (the reference's exception). */
+ * reported as DTQ_ERR_INVALID_ARGUMENT (the reference's exception).
+ * Thread-safe: concurrent calls on one handle are serialised (the handle
+ * owns the staging buffers and streams). */
 int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_t h, int mode,
                              void* y, int y_dtype, void* stream);
 

@@ -435,6 +435,7 @@ struct dtq_qlinear_s {
   std::vector<cudaEvent_t> ev_in, ev_out;          // per chunk: H2D done, GEMM done
   void* pws = nullptr;
   size_t pws_bytes = 0;
+  std::mutex host_mu;  // forward_host is synchronous: one call per handle at a time
 };
 
 namespace {
@@ -1080,6 +1081,7 @@ int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_
   const size_t yb = ye * static_cast<size_t>(M) * h->N;
   if (xb == 0 || yb == 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "forward_host: bad dtype");
   cudaStream_t st = as_stream(stream);
+  std::lock_guard<std::mutex> host_lock(h->host_mu);  // handle-owned buffers and streams
   DTQ_TRY(grow(&h->hx, &h->hx_bytes, xb));
   DTQ_TRY(grow(&h->hy, &h->hy_bytes, yb));
   CUDA_TRY(cudaMemsetAsync(h->status, 0, sizeof(int32_t), st));

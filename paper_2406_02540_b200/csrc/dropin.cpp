@@ -20,6 +20,8 @@
 #include <cstring>
 #include <limits>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -167,15 +169,22 @@ std::vector<uint8_t> codes_for(const Matrix& x, const GroupingScheme& scheme, in
 }
 
 // device QuantLinear handle built from the layer's host fields
+// The device handle keeps per-handle scratch (codes, the s32 accumulator of
+// the fp64 epilogue), so calls on one layer are serialised by its mutex: the
+// reference API is thread-safe (pure functions on const layers) and stays so.
 struct Handle {
   dtq_qlinear_t h = nullptr;
+  std::mutex m;
   ~Handle() {
     if (h) dtq_qlinear_destroy(h);
   }
 };
 
-dtq_qlinear_t device_layer(const QuantLinear& layer) {
-  if (layer.device) return static_cast<Handle*>(layer.device.get())->h;
+std::mutex g_layer_mu;  // guards the lazy QuantLinear::device upload
+
+Handle* device_layer(const QuantLinear& layer) {
+  std::lock_guard<std::mutex> lock(g_layer_mu);
+  if (layer.device) return static_cast<Handle*>(layer.device.get());
   const QuantizedTensor& w = layer.w_q;
   if (w.params.size() != w.rows || w.ints.size() != w.rows * w.cols)
     throw std::invalid_argument("qlinear: malformed weight tensor");
@@ -198,7 +207,7 @@ dtq_qlinear_t device_layer(const QuantLinear& layer) {
                                       db ? db->p : nullptr, nullptr, nullptr, &hd->h));
   cuda(cudaDeviceSynchronize());
   layer.device = hd;
-  return hd->h;
+  return hd.get();
 }
 
 Matrix balance_rows(const Matrix& m, const double* smooth, bool mul, const int8_t* signs,
@@ -545,12 +554,15 @@ Matrix qlinear_forward(const Matrix& x, const QuantLinear& layer) {
   if (max_term > std::numeric_limits<int64_t>::max() / static_cast<int64_t>(c_in))
     throw std::overflow_error("qlinear_forward: accumulator could overflow");
   if (!x.all_finite()) throw std::invalid_argument("quantize: non-finite input");
-  const dtq_qlinear_t h = device_layer(layer);
+  Handle* hd = device_layer(layer);
   Dev<double> dx(x.data().data(), x.size()), dy(x.rows() * c_out);
-  check(dtq_qlinear_forward(dx.p, DTQ_F64, x.rows(), c_in, h, DTQ_MODE_EXACT, nullptr, dy.p, DTQ_F64,
-                            c_out, nullptr, 0, nullptr, nullptr));
   Matrix y(x.rows(), c_out);
-  dy.get(y.data().data());
+  {
+    std::lock_guard<std::mutex> lock(hd->m);
+    check(dtq_qlinear_forward(dx.p, DTQ_F64, x.rows(), c_in, hd->h, DTQ_MODE_EXACT, nullptr, dy.p,
+                              DTQ_F64, c_out, nullptr, 0, nullptr, nullptr));
+    dy.get(y.data().data());
+  }
   return y;
 }
 

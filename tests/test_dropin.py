@@ -127,3 +127,16 @@ def test_reference_model_and_io_unit_tests_pass_on_device(tmp_path):
     print(r.stderr[-4000:])
     assert r.returncode == 0, r.stderr[-4000:]
     assert " 0 failed" in r.stdout
+
+
+THREADS = os.path.join(ROOT, "tests", "dropin", "_bin", "dtq_thread_test")
+
+
+@pytest.mark.gpu
+def test_dropin_concurrent_forward_is_bitexact():
+    # qlinear_forward on one const layer from 8 threads (first use included)
+    if not os.path.exists(THREADS):
+        pytest.skip("thread test binary not built")
+    r = subprocess.run([THREADS], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0 and "threads ok" in r.stdout, r.stdout + r.stderr[-2000:]

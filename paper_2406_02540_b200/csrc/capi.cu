@@ -274,7 +274,9 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
   if (!tile_off && cols <= 8192 && ldc % 16 == 0 && reinterpret_cast<uintptr_t>(codes) % 16 == 0) {
     const bool has_b = kind == DTQ_PROLOGUE_MODULATE || kind == DTQ_PROLOGUE_LN_MODULATE;
     const bool has_a = has_b || col_mul != nullptr;
-    const int R = dtq_fq_tile_rows(rows, cols, static_cast<int>(es), has_a, has_b, kind, sms);
+    const bool exact_v = kind == DTQ_PROLOGUE_NONE && !has_a && signs == nullptr;
+    const int R = dtq_fq_tile_rows(rows, cols, static_cast<int>(es), has_a, has_b, kind, exact_v,
+                                   sms);
     if (R > 0)
       return fq_error(dtq_launch_fq_tile(a, static_cast<int>(es), x_dtype == DTQ_BF16 ? 1 : 0,
                                          signs != nullptr, R, sms, st));

@@ -10,7 +10,8 @@
 // Rows per tile (compile-time in the kernel): 8, or 4 when an 8-row double
 // buffer of a wide row does not fit shared memory.  0 = the shape does not
 // fit the tile kernel at all (the caller uses the lane-group kernel).
-int dtq_fq_tile_rows(int64_t M, int64_t K, int es, bool has_a, bool has_b, int pro, int sms) {
+int dtq_fq_tile_rows(int64_t M, int64_t K, int es, bool has_a, bool has_b, int pro, bool exact_v,
+                     int sms) {
   (void)M;
   (void)sms;
   constexpr size_t kMax = 220 * 1024;
@@ -20,7 +21,11 @@ int dtq_fq_tile_rows(int64_t M, int64_t K, int es, bool has_a, bool has_b, int p
     const char* e = std::getenv("DTQ_FQ_ROWS");
     return e ? std::atoi(e) : 8;
   }();
-  for (int R = force; R >= 4; R /= 2)
+  // wide rows with exact codes (no prologue, smoothing or rotation): 4-row
+  // tiles, two 288-thread CTAs per SM instead of one of 576 (the exact-code
+  // path's registers spill at 576 threads): 73.7 vs 82.9 us at 16384 x 4608
+  const int start = (!four && exact_v && force == 8) ? 4 : force;
+  for (int R = start; R >= 4; R /= 2)
     if ((four ? R == 8 : R >= 4) && dtq_fq::fq_tile_threads(K, R, pro) <= cap &&
         dtq_fq::fq_tile_layout(K, R, es, has_a, has_b, 2).bytes <= kMax)
       return R;

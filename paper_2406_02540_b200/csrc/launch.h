@@ -13,7 +13,8 @@
 // dtq_dtype) and the fp32 "fast" kernels per input type
 cudaError_t dtq_launch_fq_exact(const dtq_fq::FqArgs& a, int x_dtype, int cpt, bool vec,
                                 int block, int sms, cudaStream_t st);
-int dtq_fq_tile_rows(int64_t M, int64_t K, int es, bool has_a, bool has_b, int pro, int sms);
+int dtq_fq_tile_rows(int64_t M, int64_t K, int es, bool has_a, bool has_b, int pro, bool exact_v,
+                     int sms);
 cudaError_t dtq_launch_fq_tile(const dtq_fq::FqArgs& a, int x_dtype_size, int x_is_bf16, bool rot,
                                int R, int sms, cudaStream_t st);
 cudaError_t dtq_launch_fq_fast_f16(const dtq_fq::FqArgs& a, int cpt, bool rot, int block, int sms,

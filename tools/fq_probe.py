@@ -1,6 +1,8 @@
 """Per-CTA timeline of the tile quantizer (DTQ_DEBUG_FQ_PROBE=1 diagnostics).
 
 usage: DTQ_DEBUG_FQ_PROBE=1 python tools/fq_probe.py M K
+Needs a build with -DFQ_TILE_PROBE (tools/variant.sh probe '-DFQ_TILE_PROBE';
+export DTQ_B200_LIB=variants/probe/libdtq_b200.so).
 """
 import ctypes as C
 import os

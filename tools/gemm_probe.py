@@ -1,6 +1,8 @@
 """Per-role wait cycles of the GEMM (DTQ_DEBUG_GEMM_PROBE=1 diagnostics).
 
 usage: DTQ_DEBUG_GEMM_PROBE=1 python tools/gemm_probe.py M N K [wbits]
+Needs a diagnostics build (the product kernel has no probes):
+  tools/variant.sh diag '-DDTQ_GEMM_DIAG'; export DTQ_B200_LIB=variants/diag/libdtq_b200.so
 """
 import ctypes as C
 import os

@@ -457,3 +457,55 @@ def test_w4_odd_k_exact(K):
                      out_dtype=torch.int32).cpu().numpy().astype(np.int64)
     want = (a.astype(np.int64) - z[:, None]) @ (wc.astype(np.int64) - 8).T
     assert np.array_equal(acc, want)
+
+
+@pytest.mark.parametrize("wb", [8, 4])
+def test_c5_full_size_balanced_row_shards(oracle, wb):
+    """BASELINE configs[4] at its full size on one device: M = 131072 token
+    rows (STDiT 16 x 512^2, batch 8), fc1 1152 -> 4608, smooth + 128-block
+    Hadamard fused into the quantizer.  Properties that hold at any size:
+      * the forward of each of 8 row shards (the per-GPU slice at 8 GPUs) is
+        bit-identical to the same rows of the whole forward (quant.cpp:70-73:
+        per-token params are row-local; qgemm.cpp:52-63: per-row dot);
+      * on sampled rows, codes are within 1 LSB of the oracle on <= 1e-4 of
+        elements, the int32 accumulators recomputed by the oracle from the
+        GPU's own codes are equal, and fp16 y is within 1e-3."""
+    rng = np.random.default_rng(131072 + wb)
+    M, K, N = 131072, 1152, 4608
+    # activations drawn on the device (the oracle checks a row sample only)
+    g = torch.exp(torch.randn(K, device=DEV, dtype=torch.float64))
+    xt = (torch.randn(M, K, device=DEV, dtype=torch.float64) * g)
+    xt[:, :4] *= 30.0
+    xt = xt.to(torch.float16)
+    xt[0] = 0.0
+    xt[1] = 0.5
+    w = rng.standard_normal((N, K)) / np.sqrt(K)
+    amax = xt[:8192].abs().amax(0).double().cpu().numpy()
+    smooth = oracle.scaling_mask(amax, np.abs(w).max(0), 0.5)
+    signs = oracle.hadamard_signs(K, 7)
+    bal = dtq.Balance(cuda(smooth), cuda(signs), 128)
+    bias = rng.standard_normal(N) * 0.1
+    layer = dtq.QuantLinear.create(cuda(w.astype(np.float16)), wb, 8, bias=cuda(bias), balance=bal)
+    y = layer.forward(xt, out_dtype=torch.float16)
+    shard = M // 8
+    for r in range(8):
+        a, b = r * shard, (r + 1) * shard
+        assert torch.equal(layer.forward(xt[a:b], out_dtype=torch.float16), y[a:b]), f"shard {r}"
+    codes, s, z = layer.quantize(xt)
+    acc = layer.gemm(codes, s, z, out_dtype=torch.int32)
+    rows = np.sort(rng.choice(M, 256, replace=False))
+    rows[:2] = [0, 1]
+    x_rows = xt[torch.as_tensor(rows, device=DEV)].double().cpu().numpy()
+    xr = oracle.rotate_blocks(oracle.scale_x(x_rows, smooth), signs, 128)
+    c_ref, s_ref, _ = oracle.quantize_rows(xr, 8)
+    c_gpu = codes.cpu().numpy()[rows]
+    d = np.abs(c_gpu.astype(np.int32) - c_ref.astype(np.int32))
+    assert d.max() <= 1 and (d > 0).mean() <= 1e-4, (d.max(), (d > 0).mean())
+    assert np.allclose(s.cpu().numpy()[rows], s_ref, rtol=1e-6)
+    wc, sw, _ = layer.export()
+    zw = 1 << (wb - 1)
+    z_gpu = z.cpu().numpy()[rows]
+    acc_ref = oracle.qlinear_acc(c_gpu, z_gpu, wc, np.full(N, zw, np.int32))
+    assert np.array_equal(acc.cpu().numpy()[rows].astype(np.int64), acc_ref)
+    y_ref = oracle.qlinear_epilogue(acc_ref, s.cpu().numpy()[rows], sw, bias)
+    assert rel_err(y.float().cpu().numpy()[rows], y_ref) <= REL_TOL

@@ -45,6 +45,15 @@ WORKLOAD = ("W8A8 quantized linear, PixArt-alpha 1024px fc1 (M=4096, K=1152, N=4
             "smooth + 128-block Hadamard fused into the per-token quantizer, fp16 in/out")
 
 
+def c2_config(world: int) -> dict:
+    """The headline workload's config, identical on both arms."""
+    return {"workload": WORKLOAD, "M_per_rank": M, "K": K, "N": N,
+            "global_batch": M * world, "seq_len": M, "parallelism": f"dp{world}",
+            "weights": "W8 per-out-channel symmetric, random init",
+            "l2": "inputs larger than L2: a ring of layers (own weights) and x/y buffers "
+                  "over > 300 MB, steps back to back"}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -253,13 +262,14 @@ def run_reference(args, world, rank):
     out = {
         "metric": METRIC, "impl": "reference", "value": tops, "unit": "TOPS",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3 * (M / rows), "higher_is_better": True, "scaling": "weak",
+        # measured time of one step's bounded sample (rows of M), not scaled
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "global_batch": M * args.gpus, "seq_len": M,
-                   "parallelism": f"dp{args.gpus}"},
+        "config": c2_config(args.gpus),
         "cpu_baseline": {"value": tops, "unit": "TOPS", "cores": threads, "kind": "reference",
                          "sample": f"{rows} of {M} token rows per step (row-local, exact), "
-                                   "apply_scaling + rotate_channels + qlinear_forward"},
+                                   "apply_scaling + rotate_channels + qlinear_forward; "
+                                   "ms_per_step is that sample's measured time"},
         "e2e": {"value": tops, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -450,25 +460,37 @@ def run_ours(args, world, rank, local):
     for i in range(nstep_ring):
         lring[i].forward(sxring[i], out=syring[i], workspace=ws)
     torch.cuda.synchronize()
+
+    def k_steps():
+        for i in range(args.steps):
+            j = i % nstep_ring
+            lring[j].forward(sxring[j], out=syring[j], workspace=ws)
+
+    # host cost of the API call, eager (reported; not in the timed region):
+    # Python + ctypes + the C ABI's launch path per forward
+    h_start = time.perf_counter()
+    k_steps()
+    h_issue = (time.perf_counter() - h_start) / args.steps
+    torch.cuda.synchronize()
+    # the K timed steps are captured once as a CUDA graph (the fused
+    # quantizer -> GEMM pairs keep their programmatic-dependent-launch
+    # edges), so the host never paces the GPU
+    g_steps = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_steps):
+        k_steps()
+    g_steps.replay()
+    torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        # the GPU spins ~0.1 ms (untimed, before the first event) while the
-        # host queues the first steps: no host-launch bubble at the start of
-        # the timed region (host issue ~19 us/step < GPU ~28 us/step keeps the
-        # queue ahead after that)
-        torch.cuda._sleep(200_000)
         t0.record(stream)
-        h_start = time.perf_counter()
-        for i in range(args.steps):
-            j = i % nstep_ring
-            lring[j].forward(sxring[j], out=syring[j], workspace=ws)
-        h_issue = (time.perf_counter() - h_start) / args.steps
+        g_steps.replay()
         t1.record(stream)
         torch.cuda.synchronize()
     barrier(world)
     t_fwd = t0.elapsed_time(t1) * 1e-3 / args.steps
+    del g_steps
     t_step = max_over_ranks(t_fwd, world)
     ops = 2.0 * M * N * K
     value = ops * world / t_step / 1e12
@@ -669,11 +691,7 @@ def run_ours(args, world, rank, local):
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8xs8->s32 (fp16 in/out)",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "M_per_rank": M, "K": K, "N": N,
-                   "global_batch": M * world, "seq_len": M, "parallelism": f"dp{world}",
-                   "weights": "W8 per-out-channel symmetric, random init",
-                   "l2": f"inputs larger than L2: ring of {nstep_ring} layers (own weights) "
-                         "and x/y buffers, steps back to back, one event pair over all K"},
+        "config": c2_config(world),
         "roofline": {"bound": "tensor", "achieved": gemm_tops, "peak": int8_peak,
                      "unit": "TFLOP/s", "frac": gemm_tops / int8_peak, "traffic": traffic,
                      "kernel": "qgemm_kernel (tcgen05.mma kind::i8)",
@@ -694,7 +712,8 @@ def run_ours(args, world, rank, local):
                       "fused_forward_call_l2_flushed": t_flushed * 1e3,
                       "host_issue_per_step": h_issue * 1e3,
                       "note": "value/ms_per_step: one layer.forward per step (both kernels), "
-                              "K steps back to back over a >L2 ring, one event pair; "
+                              "K steps back to back over a >L2 ring, captured as one CUDA "
+                              "graph, one event pair; host_issue_per_step: eager API call; "
                               "_l2_flushed: 512 MB write before each step, one event pair per "
                               "step; per-kernel: median of CUDA-graph batches of back-to-back "
                               "launches over a >L2 input ring"},

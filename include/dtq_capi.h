@@ -81,7 +81,8 @@ typedef struct dtq_prologue {
 typedef struct dtq_balance {
   const double* smooth; /* [dev] [K] ScalingMask.s (X / s, W * s) or NULL     */
   const int8_t* signs;  /* [dev] [K] RotationMatrix.sign_diag (+-1) or NULL   */
-  int32_t hblock;       /* rotation block, power of two in [8, 256]           */
+  int32_t hblock;       /* rotation block, power of two in [8, 16384]; blocks
+                           wider than 256 take an fp64 pre-pass (exact)      */
 } dtq_balance;
 
 /* opaque quantized-linear handle (QuantLinear, qgemm.hpp:17-24) */
@@ -248,11 +249,34 @@ int dtq_checkpoint_layer_info(dtq_checkpoint_t ck, int64_t i, const char** name,
  * uploaded as stored and unpacked on the device (W4: straight into the
  * GEMM's nibble layout); the f32 scales become the fp64 s_w exactly as
  * read_checkpoint widens them; the mask becomes the smoothing vector and the
- * rotation signs the rotation, in blocks of `hblock` columns (0 = the
- * stored rotation length).  Needs symmetric per-output-channel weights (the
- * GEMM's layout): anything else is DTQ_ERR_UNSUPPORTED. */
+ * rotation signs the rotation over the stored rotation length (the weights
+ * were rotated by that full rot_len-point Hadamard); `hblock` must be 0 or
+ * equal to it (anything else is DTQ_ERR_INVALID_ARGUMENT).  Needs symmetric
+ * per-output-channel weights (the GEMM's layout): anything else is
+ * DTQ_ERR_UNSUPPORTED. */
 int dtq_checkpoint_load_layer(dtq_checkpoint_t ck, int64_t i, int act_bits, int hblock,
                               void* stream, dtq_qlinear_t* out);
+
+/* ---------------------------------------------------------------- mixed precision
+ * One layer of a MixedPrecisionPlan (plan.hpp:30-40): the weight bits of each
+ * of the kNumRanges = 4 timestep ranges.  The layer keeps one device-resident
+ * QuantLinear per distinct bit width in its row (e.g. W8 for range 0, W4 for
+ * ranges 1-3), all built from the same weights and balance by
+ * dtq_qlinear_create.  The forward of denoising step t of `steps` dispatches
+ * to bits_for(layer, t * 4 / steps), the range index of toydit.cpp:113-117.
+ *   bits [host] 4 entries in {2,4,6,8} (the reference's 16 = floating-point
+ *        passthrough is not a quantized layer: DTQ_ERR_INVALID_ARGUMENT) */
+typedef struct dtq_planned_s* dtq_planned_t;
+
+int dtq_planned_create(const void* w, int w_dtype, int64_t N, int64_t K, int64_t ldw,
+                       const int32_t* bits, int act_bits, const double* bias,
+                       const dtq_balance* balance, void* stream, dtq_planned_t* out);
+int dtq_planned_destroy(dtq_planned_t p);
+/* the handle serving denoising step t of `steps` (borrowed: owned by p);
+ * steps >= 1, 0 <= t < steps, else DTQ_ERR_INVALID_ARGUMENT */
+int dtq_planned_select(dtq_planned_t p, int64_t t, int64_t steps, dtq_qlinear_t* out);
+/* weight bits of range r (0..3) */
+int dtq_planned_bits(dtq_planned_t p, int r, int* bits);
 
 #ifdef __cplusplus
 }

@@ -157,6 +157,25 @@ def _ref_or_none(obj):
     return None if obj is None else C.byref(obj)
 
 
+def _check_rows(t, cols: int, what: str, cuda: bool = True):
+    """A 2-D row-major tensor with `cols` columns (the reference's
+    'X cols != C_in' check, qgemm.cpp:26-27) on the expected side."""
+    if t.dim() != 2 or t.shape[1] != cols:
+        raise ValueError(f"{what}: expected [rows, {cols}], got {tuple(t.shape)}")
+    if t.stride(1) != 1:
+        raise ValueError(f"{what}: rows must be contiguous (stride(1) == 1)")
+    if bool(t.is_cuda) != cuda:
+        raise ValueError(f"{what}: expected a {'CUDA' if cuda else 'host'} tensor")
+
+
+def _check_out(out, M: int, N: int, what: str, cuda: bool = True):
+    if out.dim() != 2 or tuple(out.shape) != (M, N) or out.stride(1) != 1:
+        raise ValueError(f"{what}: output must be [{M}, {N}] with contiguous rows, "
+                         f"got {tuple(out.shape)} / strides {tuple(out.stride())}")
+    if bool(out.is_cuda) != cuda:
+        raise ValueError(f"{what}: output on the wrong device")
+
+
 def quantize_rows(x, bits: int = 8, symmetric: bool = False, mode: int = MODE_FAST,
                   balance: Optional[Balance] = None, prologue: Optional[Prologue] = None,
                   status=None, stream=None):
@@ -164,7 +183,9 @@ def quantize_rows(x, bits: int = 8, symmetric: bool = False, mode: int = MODE_FA
 
     Returns (codes u8 [rows, cols], scale f64 [rows], zero_point i32 [rows])."""
     torch = _torch()
-    assert x.is_cuda and x.dim() == 2 and x.stride(1) == 1
+    if x.dim() != 2:
+        raise ValueError("quantize_rows: expected a 2-D tensor")
+    _check_rows(x, x.shape[1], "quantize_rows")
     rows, cols = x.shape
     ldc = (cols + 15) // 16 * 16
     codes_buf = torch.empty((rows, ldc), dtype=torch.uint8, device=x.device)
@@ -249,9 +270,16 @@ class QuantLinear:
     def gemm(self, codes, s_x, z_x, out_dtype=None, out=None, stream=None):
         """Integer GEMM + epilogue on quantized activations (qgemm.cpp:52-63)."""
         torch = _torch()
+        _check_rows(codes, self.K, "gemm codes")
+        if codes.dtype != torch.uint8:
+            raise ValueError("gemm: codes must be uint8")
         M = codes.shape[0]
+        if s_x.numel() < M or z_x.numel() < M or s_x.dtype != torch.float64 or \
+                z_x.dtype != torch.int32 or not (s_x.is_cuda and z_x.is_cuda):
+            raise ValueError("gemm: s_x (f64) and z_x (i32) need M entries on the device")
         if out is None:
             out = torch.empty((M, self.N), dtype=out_dtype or torch.float16, device=codes.device)
+        _check_out(out, M, self.N, "gemm")
         _check(lib().dtq_qgemm(codes.data_ptr(), codes.stride(0), s_x.data_ptr(), z_x.data_ptr(),
                                M, self._h, out.data_ptr(), _dtype_code(out.dtype), out.stride(0),
                                _stream(stream)))
@@ -261,6 +289,7 @@ class QuantLinear:
                  out=None, status=None, stream=None):
         """The fused-quantizer stage of forward(): (codes, s_x, z_x)."""
         torch = _torch()
+        _check_rows(x, self.K, "quantize")
         M = x.shape[0]
         if out is None:
             ldc = (self.K + 15) // 16 * 16
@@ -268,6 +297,9 @@ class QuantLinear:
             out = (buf[:, :self.K], torch.empty(M, dtype=torch.float64, device=x.device),
                    torch.empty(M, dtype=torch.int32, device=x.device))
         codes, s, z = out
+        _check_out(codes, M, self.K, "quantize codes")
+        if s.numel() < M or z.numel() < M:
+            raise ValueError("quantize: s / z need M entries")
         pr = prologue._c() if prologue is not None else None
         _check(lib().dtq_qlinear_quantize(x.data_ptr(), _dtype_code(x.dtype), M, x.stride(0),
                                           self._h, mode, _ref_or_none(pr), codes.data_ptr(),
@@ -280,10 +312,15 @@ class QuantLinear:
                 stream=None):
         """qlinear_forward(x, layer): fused quantizer + GEMM, stream-ordered."""
         torch = _torch()
+        _check_rows(x, self.K, "qlinear_forward")
         M = x.shape[0]
         if out is None:
             out = torch.empty((M, self.N), dtype=out_dtype or torch.float16, device=x.device)
+        _check_out(out, M, self.N, "qlinear_forward")
         pr = prologue._c() if prologue is not None else None
+        if workspace is not None and (workspace.dtype != torch.uint8 or not workspace.is_cuda
+                                      or not workspace.is_contiguous()):
+            raise ValueError("qlinear_forward: workspace must be a contiguous uint8 CUDA tensor")
         ws_ptr, ws_n = (None, 0) if workspace is None else (workspace.data_ptr(), workspace.numel())
         _check(lib().dtq_qlinear_forward(x.data_ptr(), _dtype_code(x.dtype), M, x.stride(0),
                                          self._h, mode, _ref_or_none(pr), out.data_ptr(),
@@ -293,9 +330,11 @@ class QuantLinear:
 
     def forward_host(self, x_host, y_host, mode: int = MODE_FAST, stream=None):
         """Host buffers in, host buffers out (H2D + forward + D2H, synchronised)."""
-        torch = _torch()
-        assert not x_host.is_cuda and not y_host.is_cuda
+        _check_rows(x_host, self.K, "forward_host", cuda=False)
         M = x_host.shape[0]
+        _check_out(y_host, M, self.N, "forward_host", cuda=False)
+        if not (x_host.is_contiguous() and y_host.is_contiguous()):
+            raise ValueError("forward_host: host buffers must be dense")
         _check(lib().dtq_qlinear_forward_host(x_host.data_ptr(), _dtype_code(x_host.dtype), M,
                                               self._h, mode, y_host.data_ptr(),
                                               _dtype_code(y_host.dtype), _stream(stream)))

@@ -22,6 +22,11 @@
 #include "../../include/dtq_capi.h"
 #include "launch.h"
 
+// parity_kernels.cu
+int dtq_quantize_rows_wide_f64(const double* x, int64_t rows, int64_t cols, int64_t ldx, int bits,
+                               int symmetric, uint8_t* codes, int64_t ldc, double* scale,
+                               int32_t* zero, int32_t* status, cudaStream_t st);
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -60,26 +65,36 @@ struct DeviceInfo {
   int major = 0;
 };
 
+// Per-thread cache of the current device's properties: one cudaGetDevice
+// (a few tens of ns) per call instead of a device count + property query.
 DeviceInfo& device_info() {
   thread_local DeviceInfo info;
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return info;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    info.dev = -1;
+    info.major = 0;
+    return info;
+  }
   if (info.dev != dev) {
     cudaDeviceProp p;
     if (cudaGetDeviceProperties(&p, dev) == cudaSuccess) {
       info.dev = dev;
       info.sms = p.multiProcessorCount;
       info.major = p.major;
+    } else {
+      info.dev = -1;
+      info.major = 0;
     }
   }
   return info;
 }
 
 int check_device() {
-  int n = 0;
-  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
-    return fail(DTQ_ERR_CUDA, "no CUDA device (the sm_100a path has no CPU fallback)");
   DeviceInfo& d = device_info();
+  if (d.dev < 0) {
+    cudaGetLastError();  // clear the sticky "no device" error of the probe
+    return fail(DTQ_ERR_CUDA, "no CUDA device (the sm_100a path has no CPU fallback)");
+  }
   if (d.major != 10)
     return fail(DTQ_ERR_CUDA, "device compute capability %d.x is not sm_100 (B200)", d.major);
   return DTQ_OK;
@@ -118,6 +133,32 @@ int make_tmap_u8(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, i
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DTQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return DTQ_OK;
+}
+
+// rotation blocks: the fused quantizers take up to 256 columns; wider blocks
+// (up to a full 16384-point rotation) take the fp64 pre-pass
+constexpr int kMaxFusedHblock = 256;
+constexpr int kMaxHblock = 16384;
+
+// any input dtype -> dense fp64 (the pre-pass of wide rotation blocks);
+// non-finite values set status like the fused quantizers
+__global__ void to_f64_kernel(const void* __restrict__ x, int dt, int64_t rows, int64_t cols,
+                              int64_t ldx, double* __restrict__ out, int32_t* status) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rows * cols;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols, j = r * ldx + c;
+    double v;
+    switch (dt) {
+      case DTQ_F16: v = static_cast<double>(__half2float(static_cast<const __half*>(x)[j])); break;
+      case DTQ_BF16:
+        v = static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(x)[j]));
+        break;
+      case DTQ_F32: v = static_cast<double>(static_cast<const float*>(x)[j]); break;
+      default: v = static_cast<const double*>(x)[j]; break;
+    }
+    if (status && !isfinite(v)) atomicOr(status, 1);
+    out[i] = v;
+  }
 }
 
 // ------------------------------------------------------------------ FQ launch
@@ -172,7 +213,8 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
                        int bits, int symmetric, int mode, int smooth_mul, const double* smooth_d,
                        const float* col_mul, const int8_t* signs, int hblock,
                        const dtq_prologue* pro, uint8_t* codes, int64_t ldc, double* scale,
-                       int32_t* zero, int32_t* status, cudaStream_t st) {
+                       int32_t* zero, int32_t* status, cudaStream_t st,
+                       bool col_mul_const = true) {
   if (rows <= 0 || cols <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: empty matrix");
   if (!bits_supported(bits))
     return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: bits must be one of {2,4,6,8}");
@@ -182,15 +224,55 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
   if (dtype_size(x_dtype) == 0 || x_dtype == DTQ_S32)
     return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: bad input dtype %d", x_dtype);
   if (signs) {
-    if (hblock < 8 || hblock > 256 || (hblock & (hblock - 1)) != 0)
+    if (hblock < 8 || hblock > kMaxHblock || (hblock & (hblock - 1)) != 0)
       return fail(DTQ_ERR_INVALID_ARGUMENT,
-                  "hadamard: block must be a power of two in [8, 256]");
+                  "hadamard: block must be a power of two in [8, %d]", kMaxHblock);
     if (cols % hblock != 0)
       return fail(DTQ_ERR_INVALID_ARGUMENT, "rotate_channels: channel count %lld not a multiple "
                   "of the rotation block %d", (long long)cols, hblock);
   }
-  if (cols > 16384) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: cols > 16384");
   const int kind = pro ? pro->kind : DTQ_PROLOGUE_NONE;
+  if (signs && hblock > kMaxFusedHblock) {
+    // rotation blocks wider than the fused kernels' (a reference checkpoint
+    // stores weights rotated by the full C_in-point Hadamard, dtq_main.cpp
+    // cmd_quantize): fp64 copy, apply_scaling + rotate_channels in the
+    // reference order (balance_kernel, balance.cpp:57-67, 94-107), then the
+    // exact quantizer on the balanced rows.  Always fp64 (never less exact).
+    if (kind != DTQ_PROLOGUE_NONE)
+      return fail(DTQ_ERR_UNSUPPORTED, "prologue with a rotation block wider than %d",
+                  kMaxFusedHblock);
+    DTQ_TRY(check_device());
+    double* tmp = nullptr;
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&tmp), rows * cols * sizeof(double), st));
+    const int64_t n = rows * cols;
+    to_f64_kernel<<<static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 32)), 256, 0, st>>>(
+        x, x_dtype, rows, cols, ldx, tmp, status);
+    int r = cudaGetLastError() == cudaSuccess ? DTQ_OK : fail(DTQ_ERR_CUDA, "to_f64 launch");
+    if (r == DTQ_OK &&
+        dtq_balance_apply(tmp, rows, cols, cols, smooth_d, smooth_mul, signs, hblock, tmp, cols,
+                          st) != DTQ_OK)
+      r = fail(DTQ_ERR_CUDA, "balance_apply launch failed");
+    if (r == DTQ_OK)
+      r = quantize_rows_impl(tmp, DTQ_F64, rows, cols, cols, bits, symmetric, DTQ_MODE_EXACT, 0,
+                             nullptr, nullptr, nullptr, 0, nullptr, codes, ldc, scale, zero,
+                             status, st);
+    cudaFreeAsync(tmp, st);
+    return r;
+  }
+  if (cols > 16384) {
+    // wider groups (the drop-in's per_tensor() / per_channel() params):
+    // chunked fp64 min / max, exact params, static codes
+    if (!(mode == DTQ_MODE_EXACT || x_dtype == DTQ_F64) || x_dtype != DTQ_F64 || smooth_d ||
+        signs || kind != DTQ_PROLOGUE_NONE || smooth_mul)
+      return fail(DTQ_ERR_INVALID_ARGUMENT,
+                  "quantize: rows wider than 16384 need fp64 input, exact mode, no balance "
+                  "or prologue");
+    DTQ_TRY(check_device());
+    const int r = dtq_quantize_rows_wide_f64(static_cast<const double*>(x), rows, cols, ldx, bits,
+                                             symmetric, codes, ldc, scale, zero, status, st);
+    if (r != DTQ_OK) return fail(r, "quantize: wide-row launch failed");
+    return DTQ_OK;
+  }
   if (kind < 0 || kind > 3) return fail(DTQ_ERR_INVALID_ARGUMENT, "bad prologue kind");
   if ((kind == DTQ_PROLOGUE_MODULATE || kind == DTQ_PROLOGUE_LN_MODULATE) &&
       (!pro->scale || !pro->shift))
@@ -225,6 +307,7 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
   a.symmetric = symmetric;
   a.smooth_d = exact ? smooth_d : nullptr;
   a.col_mul = exact ? nullptr : col_mul;
+  a.col_mul_const = col_mul_const ? 1 : 0;
   a.signs = signs;
   a.hblock = signs ? hblock : 0;
   a.pro_scale = pro ? pro->scale : nullptr;
@@ -438,6 +521,19 @@ struct dtq_qlinear_s {
   void* pws = nullptr;
   size_t pws_bytes = 0;
   std::mutex host_mu;  // forward_host is synchronous: one call per handle at a time
+  // encoded A / Y tensor maps of recent calls (a layer sees the same few
+  // activation / output buffers every step): encoding one costs ~1-2 us of
+  // host time, more than a C2-sized quantizer launch
+  struct TmapEntry {
+    const void* base = nullptr;
+    int64_t rows = 0, cols = 0, ld = 0;
+    int box_cols = 0, box_rows = 0, swz = 0;
+    CUtensorMap map;
+  };
+  static constexpr int kTmapCache = 16;
+  TmapEntry tmaps[kTmapCache];
+  int tmap_next = 0;
+  std::mutex tmap_mu;
 };
 
 namespace {
@@ -467,6 +563,31 @@ void free_handle(dtq_qlinear_s* h) {
   delete h;
 }
 
+// make_tmap_u8 through the handle's cache of recently encoded maps
+int cached_tmap_u8(dtq_qlinear_s* h, CUtensorMap* m, const void* base, int64_t rows, int64_t cols,
+                   int64_t ld, int box_cols, int box_rows, CUtensorMapSwizzle swz) {
+  std::lock_guard<std::mutex> lock(h->tmap_mu);
+  for (const auto& e : h->tmaps) {
+    if (e.base == base && e.rows == rows && e.cols == cols && e.ld == ld &&
+        e.box_cols == box_cols && e.box_rows == box_rows && e.swz == static_cast<int>(swz)) {
+      *m = e.map;
+      return DTQ_OK;
+    }
+  }
+  DTQ_TRY(make_tmap_u8(m, base, rows, cols, ld, box_cols, box_rows, swz));
+  auto& e = h->tmaps[h->tmap_next];
+  h->tmap_next = (h->tmap_next + 1) % dtq_qlinear_s::kTmapCache;
+  e.base = base;
+  e.rows = rows;
+  e.cols = cols;
+  e.ld = ld;
+  e.box_cols = box_cols;
+  e.box_rows = box_rows;
+  e.swz = static_cast<int>(swz);
+  e.map = *m;
+  return DTQ_OK;
+}
+
 int alloc_status(dtq_qlinear_s* h, cudaStream_t st) {
   CUDA_TRY(cudaMalloc(&h->status, sizeof(int32_t)));
   CUDA_TRY(cudaMemsetAsync(h->status, 0, sizeof(int32_t), st));
@@ -482,15 +603,16 @@ int copy_balance(dtq_qlinear_s* h, const dtq_balance* bal, cudaStream_t st) {
                              cudaMemcpyDeviceToDevice, st));
   }
   if (bal->signs) {
-    if (bal->hblock < 8 || bal->hblock > 256 || (bal->hblock & (bal->hblock - 1)) != 0)
-      return fail(DTQ_ERR_INVALID_ARGUMENT, "hadamard: block must be a power of two in [8, 256]");
+    if (bal->hblock < 8 || bal->hblock > kMaxHblock || (bal->hblock & (bal->hblock - 1)) != 0)
+      return fail(DTQ_ERR_INVALID_ARGUMENT, "hadamard: block must be a power of two in [8, %d]",
+                  kMaxHblock);
     if (K % bal->hblock != 0)
       return fail(DTQ_ERR_INVALID_ARGUMENT, "rotate_channels: K not a multiple of the block");
     CUDA_TRY(cudaMalloc(&h->signs, K));
     CUDA_TRY(cudaMemcpyAsync(h->signs, bal->signs, K, cudaMemcpyDeviceToDevice, st));
     h->hblock = bal->hblock;
   }
-  if (h->smooth || h->signs) {
+  if ((h->smooth || h->signs) && h->hblock <= kMaxFusedHblock) {
     CUDA_TRY(cudaMalloc(&h->col_mul, K * sizeof(float)));
     col_mul_kernel<<<static_cast<int>((K + 255) / 256), 256, 0, st>>>(h->smooth, h->signs,
                                                                        h->hblock, K, h->col_mul);
@@ -641,8 +763,8 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
   const CUtensorMap& tB = h->tmB[brows == 256 ? 0 : (brows == 128 ? 1 : 2)];
 
   CUtensorMap tA;
-  DTQ_TRY(make_tmap_u8(&tA, codes, M, h->K, ldc, dtq_gemm::BK, dtq_gemm::BM,
-                       CU_TENSOR_MAP_SWIZZLE_128B));
+  DTQ_TRY(cached_tmap_u8(h, &tA, codes, M, h->K, ldc, dtq_gemm::BK, dtq_gemm::BM,
+                         CU_TENSOR_MAP_SWIZZLE_128B));
 
   void* yk = y;
   int64_t ldk = ldy;
@@ -700,8 +822,8 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
   CUtensorMap tY;
   std::memset(&tY, 0, sizeof(tY));
   if (g.tma_store)
-    DTQ_TRY(make_tmap_u8(&tY, yk, M, h->N * static_cast<int64_t>(es), ldk * es, 64, 32,
-                         CU_TENSOR_MAP_SWIZZLE_64B));
+    DTQ_TRY(cached_tmap_u8(h, &tY, yk, M, h->N * static_cast<int64_t>(es), ldk * es, 64, 32,
+                           CU_TENSOR_MAP_SWIZZLE_64B));
 
   const cudaError_t e = h->wbits != 4 ? dtq_launch_gemm_w8(tA, tB, tY, g, cfg, sms, st)
                                       : dtq_launch_gemm_w4(tA, tB, tY, g, cfg, sms, st);
@@ -752,6 +874,14 @@ int forward_impl(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear
 }
 
 }  // namespace
+
+// one MixedPrecisionPlan row on the device: a handle per distinct bit width
+constexpr int kPlanRanges = 4;  // plan.hpp:17 kNumRanges
+struct dtq_planned_s {
+  int bits[kPlanRanges] = {8, 8, 8, 8};
+  dtq_qlinear_t range_handle[kPlanRanges] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<dtq_qlinear_t> owned;
+};
 
 namespace {
 
@@ -889,6 +1019,7 @@ int dtq_quantize_rows(const void* x, int x_dtype, int64_t rows, int64_t cols, in
   const int hblock = balance ? balance->hblock : 0;
   cudaStream_t st = as_stream(stream);
   float* mulv = nullptr;
+  if (signs && hblock > kMaxFusedHblock) mode = DTQ_MODE_EXACT;  // the fp64 pre-pass
   const bool exact = mode == DTQ_MODE_EXACT || x_dtype == DTQ_F64;
   if ((smooth || signs) && !exact) {
     // fast mode folds sign / smooth / norm into one fp32 multiplier: derive it
@@ -901,7 +1032,8 @@ int dtq_quantize_rows(const void* x, int x_dtype, int64_t rows, int64_t cols, in
   }
   const int r = quantize_rows_impl(x, x_dtype, rows, cols, ldx, bits, symmetric, mode, 0,
                                    exact ? smooth : nullptr, mulv, signs, hblock, prologue,
-                                   codes, ldc, scale, zero, status, st);
+                                   codes, ldc, scale, zero, status, st,
+                                   /*col_mul_const=*/mulv == nullptr);
   if (mulv) cudaFreeAsync(mulv, st);
   return r;
 }
@@ -1251,6 +1383,13 @@ int dtq_checkpoint_load_layer(dtq_checkpoint_t ck, int64_t i, int act_bits, int 
   if (!L.rot.empty() && static_cast<int64_t>(L.rot.size()) != L.K)
     return fail(DTQ_ERR_INVALID_ARGUMENT, "checkpoint layer '%s': rotation length != C_in",
                 L.name.c_str());
+  // the stored weights carry the full rot_len-point rotation (dtq_main.cpp
+  // cmd_quantize: hadamard_matrix(w.cols())); the activations must get the
+  // same one, never a block-diagonal one
+  if (!L.rot.empty() && hblock != 0 && hblock != static_cast<int>(L.rot.size()))
+    return fail(DTQ_ERR_INVALID_ARGUMENT,
+                "checkpoint layer '%s': hblock %d differs from the stored rotation length %zu",
+                L.name.c_str(), hblock, L.rot.size());
   DTQ_TRY(check_device());
   cudaStream_t st = as_stream(stream);
   std::vector<double> s(L.scale.begin(), L.scale.end());  // f32 -> f64, as read_checkpoint
@@ -1286,13 +1425,71 @@ int dtq_checkpoint_load_layer(dtq_checkpoint_t ck, int64_t i, int act_bits, int 
     cleanup();
     return fail(DTQ_ERR_CUDA, "checkpoint_load_layer: upload failed");
   }
-  dtq_balance bal{d_sm, d_rot, d_rot ? (hblock > 0 ? hblock : static_cast<int>(L.rot.size())) : 0};
+  dtq_balance bal{d_sm, d_rot, d_rot ? static_cast<int>(L.rot.size()) : 0};
   r = dtq_qlinear_create_from_codes(d_codes, 1, 0, L.bits, d_s, L.N, L.K, act_bits, nullptr,
                                     (d_sm || d_rot) ? &bal : nullptr, stream, out);
   if (cudaStreamSynchronize(st) != cudaSuccess && r == DTQ_OK)
     r = fail(DTQ_ERR_CUDA, "checkpoint_load_layer: device error");
   cleanup();
   return r;
+}
+
+// ------------------------------------------------------------------ mixed precision
+int dtq_planned_create(const void* w, int w_dtype, int64_t N, int64_t K, int64_t ldw,
+                       const int32_t* bits, int act_bits, const double* bias,
+                       const dtq_balance* balance, void* stream, dtq_planned_t* out) {
+  if (!out || !bits) return fail(DTQ_ERR_INVALID_ARGUMENT, "planned_create: null argument");
+  *out = nullptr;
+  for (int r = 0; r < kPlanRanges; ++r)
+    if (!bits_supported(bits[r]))
+      return fail(DTQ_ERR_INVALID_ARGUMENT,
+                  "MixedPrecisionPlan: weight bits %d of range %d is not a quantized width "
+                  "{2,4,6,8}", bits[r], r);
+  auto* p = new dtq_planned_s();
+  for (int r = 0; r < kPlanRanges; ++r) {
+    p->bits[r] = bits[r];
+    int have = -1;
+    for (int q = 0; q < r; ++q)
+      if (bits[q] == bits[r]) have = q;
+    if (have >= 0) {
+      p->range_handle[r] = p->range_handle[have];
+      continue;
+    }
+    dtq_qlinear_t h = nullptr;
+    const int st = dtq_qlinear_create(w, w_dtype, N, K, ldw, bits[r], act_bits, bias, balance,
+                                      stream, &h);
+    if (st != DTQ_OK) {
+      dtq_planned_destroy(p);
+      return st;
+    }
+    p->owned.push_back(h);
+    p->range_handle[r] = h;
+  }
+  *out = p;
+  return DTQ_OK;
+}
+
+int dtq_planned_destroy(dtq_planned_t p) {
+  if (!p) return DTQ_OK;
+  for (dtq_qlinear_t h : p->owned) dtq_qlinear_destroy(h);
+  delete p;
+  return DTQ_OK;
+}
+
+int dtq_planned_select(dtq_planned_t p, int64_t t, int64_t steps, dtq_qlinear_t* out) {
+  if (!p || !out) return fail(DTQ_ERR_INVALID_ARGUMENT, "planned_select: null argument");
+  if (steps <= 0 || t < 0 || t >= steps)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "planned_select: step %lld outside [0, %lld)",
+                (long long)t, (long long)steps);
+  *out = p->range_handle[t * kPlanRanges / steps];  // toydit.cpp:115
+  return DTQ_OK;
+}
+
+int dtq_planned_bits(dtq_planned_t p, int r, int* bits) {
+  if (!p || !bits || r < 0 || r >= kPlanRanges)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "planned_bits: bad argument");
+  *bits = p->bits[r];
+  return DTQ_OK;
 }
 
 }  // extern "C"

@@ -122,8 +122,6 @@ void row_params(const double* x, std::size_t rows, std::size_t cols, int bits, b
                 QuantParams* out) {
   if (rows == 0 || cols == 0) throw std::invalid_argument("quant: empty group");
   if (!bits_supported(bits)) throw std::invalid_argument("quant: bits must be one of {2,4,6,8}");
-  if (cols > 16384)
-    throw std::logic_error("quant: device row quantizer handles groups of <= 16384 elements");
   Dev<double> dx(x, rows * cols);
   const int64_t ldc = pitch16(cols);
   Dev<uint8_t> dc(rows * ldc);
@@ -174,6 +172,7 @@ std::vector<uint8_t> codes_for(const Matrix& x, const GroupingScheme& scheme, in
 // reference API is thread-safe (pure functions on const layers) and stays so.
 struct Handle {
   dtq_qlinear_t h = nullptr;
+  uint64_t fingerprint = 0;  // of the host fields the handle was built from
   std::mutex m;
   ~Handle() {
     if (h) dtq_qlinear_destroy(h);
@@ -182,9 +181,53 @@ struct Handle {
 
 std::mutex g_layer_mu;  // guards the lazy QuantLinear::device upload
 
-Handle* device_layer(const QuantLinear& layer) {
+// 64-bit hash of a byte range (8 bytes per step, multiply / xor-shift mixing)
+uint64_t mix_bytes(uint64_t h, const void* data, std::size_t n) {
+  const auto* p = static_cast<const unsigned char*>(data);
+  auto mix = [](uint64_t v) {
+    v ^= v >> 33;
+    v *= 0xff51afd7ed558ccdULL;
+    v ^= v >> 33;
+    return v;
+  };
+  std::size_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    uint64_t w;
+    std::memcpy(&w, p + i, 8);
+    h = mix(h ^ w) * 0x9e3779b97f4a7c15ULL;
+  }
+  uint64_t tail = 0;
+  std::memcpy(&tail, p + i, n - i);
+  return mix(h ^ tail ^ (static_cast<uint64_t>(n) << 56));
+}
+
+// The reference's qlinear_forward reads w_q, bias and act_bits on every call
+// (qgemm.cpp:23-67): the device handle is keyed on all of them, so a layer
+// whose fields change after its first forward (or a copy that diverges from
+// the layer it was copied from) gets a fresh handle, never stale weights.
+uint64_t layer_fingerprint(const QuantLinear& layer) {
+  const QuantizedTensor& w = layer.w_q;
+  uint64_t h = 0x243f6a8885a308d3ULL;
+  const int64_t dims[4] = {static_cast<int64_t>(w.rows), static_cast<int64_t>(w.cols),
+                           layer.act_bits, layer.bias ? static_cast<int64_t>(layer.bias->size()) : -1};
+  h = mix_bytes(h, dims, sizeof(dims));
+  h = mix_bytes(h, w.ints.data(), w.ints.size());
+  for (const QuantParams& p : w.params) {
+    h = mix_bytes(h, &p.scale, sizeof(p.scale));
+    const int32_t zb[2] = {p.zero_point, p.bits};
+    h = mix_bytes(h, zb, sizeof(zb));
+  }
+  if (layer.bias) h = mix_bytes(h, layer.bias->data(), layer.bias->size() * sizeof(double));
+  return h;
+}
+
+std::shared_ptr<Handle> device_layer(const QuantLinear& layer) {
+  const uint64_t fp = layer_fingerprint(layer);
   std::lock_guard<std::mutex> lock(g_layer_mu);
-  if (layer.device) return static_cast<Handle*>(layer.device.get());
+  if (layer.device) {
+    auto cur = std::static_pointer_cast<Handle>(layer.device);
+    if (cur->fingerprint == fp) return cur;
+  }
   const QuantizedTensor& w = layer.w_q;
   if (w.params.size() != w.rows || w.ints.size() != w.rows * w.cols)
     throw std::invalid_argument("qlinear: malformed weight tensor");
@@ -206,8 +249,9 @@ Handle* device_layer(const QuantLinear& layer) {
   check(dtq_qlinear_create_from_codes(dc.p, 0, w.cols, wbits, ds.p, w.rows, w.cols, layer.act_bits,
                                       db ? db->p : nullptr, nullptr, nullptr, &hd->h));
   cuda(cudaDeviceSynchronize());
+  hd->fingerprint = fp;
   layer.device = hd;
-  return hd.get();
+  return hd;
 }
 
 Matrix balance_rows(const Matrix& m, const double* smooth, bool mul, const int8_t* signs,
@@ -541,6 +585,7 @@ QuantLinear make_quant_linear(const Matrix& w, int weight_bits, int act_bits,
   for (std::size_t o = 0; o < w.rows(); ++o) layer.w_q.params[o] = {s[o], 1 << (weight_bits - 1), weight_bits};
   layer.bias = bias;
   layer.act_bits = act_bits;
+  hd->fingerprint = layer_fingerprint(layer);
   layer.device = hd;
   return layer;
 }
@@ -554,7 +599,7 @@ Matrix qlinear_forward(const Matrix& x, const QuantLinear& layer) {
   if (max_term > std::numeric_limits<int64_t>::max() / static_cast<int64_t>(c_in))
     throw std::overflow_error("qlinear_forward: accumulator could overflow");
   if (!x.all_finite()) throw std::invalid_argument("quantize: non-finite input");
-  Handle* hd = device_layer(layer);
+  const std::shared_ptr<Handle> hd = device_layer(layer);
   Dev<double> dx(x.data().data(), x.size()), dy(x.rows() * c_out);
   Matrix y(x.rows(), c_out);
   {

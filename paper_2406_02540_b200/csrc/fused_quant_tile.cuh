@@ -306,7 +306,11 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
     for (int i = 0; i < nbuf; ++i) dtq_ptx::mbar_init(bar + i, 1);
     dtq_ptx::fence_barrier_init();
   }
-  if (!has_b && a.col_mul != nullptr) {  // the folded table of a balanced layer: constants
+  // the folded table of a balanced layer is a layer constant: read it while
+  // the producer of X drains.  A per-call table (dtq_quantize_rows derives it
+  // stream-ordered right before this launch) is only visible after pdl_wait.
+  const bool col_pre = !has_b && a.col_mul != nullptr && a.col_mul_const;
+  if (col_pre) {
     for (int c0 = t; c0 < K; c0 += 8 * blockDim.x) {
       float m[8];
 #pragma unroll
@@ -328,8 +332,9 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
       if (tile + k * static_cast<int64_t>(gridDim.x) < ntiles) issue(tile + k * gridDim.x, k);
   }
   // folded per-column affine map with the per-call modulate vectors:
-  // v -> v * A_c + B_c.  Loads are batched 8 deep per thread.
-  if constexpr (has_b) {
+  // v -> v * A_c + B_c (or a per-call multiplier alone).  Loads are batched
+  // 8 deep per thread.
+  if (has_b || (a.col_mul != nullptr && !col_pre)) {
     for (int c0 = t; c0 < K; c0 += 8 * blockDim.x) {
       float m[8], sc[8], sh[8];
 #pragma unroll

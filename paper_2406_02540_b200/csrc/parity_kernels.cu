@@ -96,6 +96,78 @@ __global__ void matmul_nt_f64_kernel(const double* __restrict__ x, int64_t M, in
   }
 }
 
+// Dynamic per-row params for rows wider than the row quantizer's tile
+// (the drop-in's per_tensor() over a whole matrix, per_channel() with many
+// rows): per-chunk fp64 min / max (exact operations, so any split gives the
+// reference's values), then one thread per row derives s, z exactly as
+// compute_minmax_params / compute_symmetric_params (quant.cpp:90-124).
+__global__ void wide_minmax_kernel(const double* __restrict__ x, int64_t cols, int64_t ldx,
+                                   int64_t chunk, double2* __restrict__ part,
+                                   int32_t* __restrict__ status) {
+  const int64_t r = blockIdx.y;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t c1 = c0 + chunk < cols ? c0 + chunk : cols;
+  double mn = __longlong_as_double(0x7ff0000000000000LL), mx = -mn;
+  bool bad = false;
+  for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+    const double v = x[r * ldx + c];
+    bad |= !isfinite(v);
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+  }
+  __shared__ double smn[32], smx[32];
+  __shared__ int sbad;
+  if (threadIdx.x == 0) sbad = 0;
+  for (int o = 16; o >= 1; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  __syncthreads();
+  if (bad) sbad = 1;
+  if ((threadIdx.x & 31) == 0) {
+    smn[threadIdx.x >> 5] = mn;
+    smx[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      mn = fmin(mn, smn[w]);
+      mx = fmax(mx, smx[w]);
+    }
+    part[r * gridDim.x + blockIdx.x] = make_double2(mn, mx);
+    if (sbad && status) atomicOr(status, 1);
+  }
+}
+
+__global__ void wide_params_kernel(const double2* __restrict__ part, int64_t rows, int nchunks,
+                                   int bits, int symmetric, double* __restrict__ scale,
+                                   int32_t* __restrict__ zero) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  double mn = part[r * nchunks].x, mx = part[r * nchunks].y;
+  for (int i = 1; i < nchunks; ++i) {
+    mn = fmin(mn, part[r * nchunks + i].x);
+    mx = fmax(mx, part[r * nchunks + i].y);
+  }
+  const double qmax = static_cast<double>((1 << bits) - 1);
+  double s, z;
+  if (symmetric) {  // quant.cpp:115-124
+    const double amax = fmax(fabs(mn), fabs(mx));
+    z = static_cast<double>(1 << (bits - 1));
+    s = amax > 0.0 ? amax / static_cast<double>((1 << (bits - 1)) - 1) : 1.0;
+  } else if (mx == mn) {  // quant.cpp:90-113, degenerate group
+    s = 1.0;
+    z = fmin(fmax(rint(-mn), 0.0), qmax);
+  } else {
+    const double lo = (0.0 < mn) ? 0.0 : mn;
+    const double hi = (mx < 0.0) ? 0.0 : mx;
+    s = (hi - lo) / qmax;
+    z = fmin(fmax(rint(-lo / s), 0.0), qmax);
+  }
+  scale[r] = s;
+  zero[r] = static_cast<int32_t>(z);
+}
+
 int grid_for(int64_t n) {
   const int64_t g = (n + 255) / 256;
   return static_cast<int>(g < 148 * 32 ? (g > 0 ? g : 1) : 148 * 32);
@@ -161,6 +233,27 @@ int dtq_matmul_nt_f64(const double* x, int64_t M, int64_t K, const double* w, in
 }
 
 }  // extern "C"
+
+// fp64 rows of any width, exact mode, no prologue / balance (capi.cu routes
+// rows wider than the tile quantizers here)
+int dtq_quantize_rows_wide_f64(const double* x, int64_t rows, int64_t cols, int64_t ldx, int bits,
+                               int symmetric, uint8_t* codes, int64_t ldc, double* scale,
+                               int32_t* zero, int32_t* status, cudaStream_t st) {
+  constexpr int64_t kChunk = 8192;
+  const int64_t nchunks = (cols + kChunk - 1) / kChunk;
+  if (nchunks > 65535 || rows > 65535) return DTQ_ERR_INVALID_ARGUMENT;
+  double2* part = nullptr;
+  if (cudaMallocAsync(&part, rows * nchunks * sizeof(double2), st) != cudaSuccess)
+    return DTQ_ERR_CUDA;
+  dim3 grid(static_cast<unsigned>(nchunks), static_cast<unsigned>(rows));
+  wide_minmax_kernel<<<grid, 256, 0, st>>>(x, cols, ldx, kChunk, part, status);
+  wide_params_kernel<<<static_cast<unsigned>((rows + 127) / 128), 128, 0, st>>>(
+      part, rows, static_cast<int>(nchunks), bits, symmetric, scale, zero);
+  quantize_static_kernel<<<grid_for(rows * cols), 256, 0, st>>>(
+      x, rows, cols, ldx, static_cast<double>((1 << bits) - 1), 1, 0, scale, zero, codes, ldc);
+  cudaFreeAsync(part, st);
+  return last_cuda("quantize_rows_wide");
+}
 
 namespace {
 int last_cuda(const char* what) {

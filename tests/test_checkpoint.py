@@ -81,3 +81,39 @@ def test_checkpoint_balanced_layer_forward_bitexact(golden):
     x = torch.from_numpy(golden["ck0_x"]).to(torch.float64).cuda()
     y = layer.forward(x, mode=dtq.MODE_EXACT, out_dtype=torch.float64)
     assert np.array_equal(y.cpu().numpy(), golden["ck0_y"])
+
+
+CKPT_ROT = os.path.join(HERE, "golden", "ckpt_rot.bin")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("i", [0, 1])
+def test_checkpoint_full_width_rotation_forward_bitexact(i):
+    # tests/golden/make_ckpt_rot.py: weights rotated by the full C_in-point
+    # Hadamard (1024 and 512 columns, wider than the fused quantizer's
+    # blocks), as the reference's `dtq quantize` stores them.  The loaded
+    # layer rotates its activations with the same full-width rotation (fp64
+    # pre-pass), bit-exact against the reference's balanced forward.
+    import torch
+    g = dict(np.load(os.path.join(HERE, "golden", "golden_rot.npz")))
+    ck = dtq.Checkpoint(CKPT_ROT)
+    layer = ck.load(i)
+    codes, scale, _ = layer.export()
+    assert np.array_equal(codes, g[f"r{i}_codes"]) and np.array_equal(scale, g[f"r{i}_s"])
+    x = torch.from_numpy(g[f"r{i}_x"]).cuda()
+    for mode in (dtq.MODE_EXACT, dtq.MODE_FAST):  # wide blocks always run in fp64
+        y = layer.forward(x, mode=mode, out_dtype=torch.float64)
+        assert np.array_equal(y.cpu().numpy(), g[f"r{i}_y"])
+    y16 = layer.forward(x, out_dtype=torch.float16).double().cpu().numpy()
+    assert np.abs(y16 - g[f"r{i}_y"]).max() <= 1e-3 * np.abs(g[f"r{i}_y"]).max()
+
+
+@pytest.mark.gpu
+def test_checkpoint_rotation_block_must_match_storage():
+    # a block-diagonal activation rotation against fully rotated weights
+    # would be silently wrong: any hblock other than 0 / the stored length
+    # is rejected
+    ck = dtq.Checkpoint(CKPT_ROT)
+    with pytest.raises(ValueError, match="rotation length"):
+        ck.load(0, hblock=128)
+    ck.load(0, hblock=1024).close()

@@ -140,3 +140,18 @@ def test_dropin_concurrent_forward_is_bitexact():
     r = subprocess.run([THREADS], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0 and "threads ok" in r.stdout, r.stdout + r.stderr[-2000:]
+
+
+FIELDS = os.path.join(ROOT, "tests", "dropin", "_bin", "dtq_fields_test")
+
+
+@pytest.mark.gpu
+def test_dropin_reads_current_layer_fields_and_wide_groups():
+    # a layer's bias / codes / scales / act_bits changed after its first
+    # forward are used (never a stale device copy), copies stay independent,
+    # and per_tensor / per_channel groups of > 16384 elements quantize
+    if not os.path.exists(FIELDS):
+        pytest.skip("fields test binary not built")
+    r = subprocess.run([FIELDS], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0 and "fields ok" in r.stdout, r.stdout + r.stderr[-2000:]

@@ -79,29 +79,74 @@ def test_random_case(oracle, i):
         y = layer.forward(xt, out_dtype=ydt).double().cpu().numpy()[rows]
         y_ref = oracle.qlinear_epilogue(acc_ref, s_ref[rows], sw)
         err = np.abs(y - y_ref).max() / max(np.abs(y_ref).max(), 1e-30)
+        # fp16 / fp32 out: the reference's 1e-3 norm (test_qgemm.cpp:19-26),
+        # balanced (fast fp32 transforms) or not; bf16 out: its own rounding
+        # (2^-9 relative per element)
         tol = 4e-3 if ydt == torch.bfloat16 else 1e-3
-        assert err <= tol + (2e-3 if balance else 0.0), (ydt, err)
+        assert err <= tol, (ydt, err)
 
 
-@pytest.mark.parametrize("i", range(16))
-def test_random_fast_balanced(oracle, i):
-    # the fast fp32 quantizer with smoothing + rotation against the oracle's
-    # fp64 scale + rotate + quantize: codes within 1 LSB, and rarely off
+FAST_CASES = 24
+
+
+def _fast_case(i):
     rng = np.random.default_rng(5000 + i)
     M = int(rng.choice([3, 64, 500, 2048]))
     K = int(rng.choice([128, 256, 1152, 2304, 4608]))
     dtype = [torch.float16, torch.bfloat16, torch.float32][int(rng.integers(0, 3))]
-    x = rng.standard_normal((M, K)) * np.exp(rng.standard_normal(K))
-    xt = torch.from_numpy(x).to(dtype).to(DEV)
-    xd = xt.double().cpu().numpy()
-    smooth = np.exp(0.3 * rng.standard_normal(K))
-    signs = dtq.hadamard_signs(K, 7)
-    bal = dtq.Balance(torch.from_numpy(smooth).to(DEV), torch.from_numpy(signs).to(DEV), 128)
-    codes, s, z = dtq.quantize_rows(xt, mode=dtq.MODE_FAST, balance=bal)
-    c_ref, s_ref, z_ref = oracle.quantize_rows(
-        oracle.rotate_blocks(oracle.scale_x(xd, smooth), signs, 128), 8)
-    d = np.abs(codes.cpu().numpy().astype(int) - c_ref.astype(int))
-    assert d.max() <= 1
-    assert (d > 0).mean() <= 1e-3
-    # the per-token scale is the reference's fp64 s of the row's fp32 range
-    assert np.allclose(s.cpu().numpy(), s_ref, rtol=1e-5, atol=0)
+    pro = ["none", "modulate", "gelu", "ln_modulate"][i % 4]
+    return rng, M, K, dtype, pro
+
+
+def _fast_chain(oracle, xd, pro, sc, sh, smooth, signs, eps=1e-6):
+    # the fp64 chain the fast kernel approximates: prologue (toydit.cpp:
+    # 339-369 modulate, :83 GELU, or the fp64 LayerNorm restatement -- no
+    # reference LN exists), apply_scaling X / s (balance.cpp:57-67), 128-block
+    # rotate_channels (balance.cpp:94-107)
+    if pro == "gelu":
+        xd = oracle.gelu(xd)
+    elif pro == "modulate":
+        xd = oracle.modulate(xd, sc, sh)
+    elif pro == "ln_modulate":
+        mu = xd.mean(1, keepdims=True)
+        var = ((xd - mu) ** 2).mean(1, keepdims=True)
+        xd = oracle.modulate((xd - mu) / np.sqrt(var + eps), sc, sh)
+    return oracle.rotate_blocks(oracle.scale_x(xd, smooth), signs, 128)
+
+
+def test_random_fast_balanced_pooled(oracle):
+    # The fast fp32 quantizer with smoothing + rotation (and each fused
+    # prologue) against the oracle's fp64 chain, over seeded cases: codes
+    # within 1 LSB everywhere, and at most 1e-4 of codes off (north_star),
+    # both per case (a case smaller than 1e4 codes may have one) and pooled.
+    nd_all, n_all, lines = 0, 0, []
+    for i in range(FAST_CASES):
+        rng, M, K, dtype, pro = _fast_case(i)
+        x = rng.standard_normal((M, K)) * np.exp(rng.standard_normal(K))
+        xt = torch.from_numpy(x).to(dtype).to(DEV)
+        xd = xt.double().cpu().numpy()
+        smooth = np.exp(0.3 * rng.standard_normal(K))
+        signs = dtq.hadamard_signs(K, 7)
+        sc = (rng.standard_normal(K) * 0.2).astype(np.float32)
+        sh = (rng.standard_normal(K) * 0.1).astype(np.float32)
+        bal = dtq.Balance(torch.from_numpy(smooth).to(DEV), torch.from_numpy(signs).to(DEV), 128)
+        kind = {"none": dtq.PROLOGUE_NONE, "modulate": dtq.PROLOGUE_MODULATE,
+                "gelu": dtq.PROLOGUE_GELU, "ln_modulate": dtq.PROLOGUE_LN_MODULATE}[pro]
+        p = dtq.Prologue(kind, torch.from_numpy(sc).to(DEV), torch.from_numpy(sh).to(DEV), 1e-6)
+        codes, s, z = dtq.quantize_rows(xt, mode=dtq.MODE_FAST, balance=bal, prologue=p)
+        ref = _fast_chain(oracle, xd, pro, sc.astype(np.float64), sh.astype(np.float64), smooth,
+                          signs)
+        c_ref, s_ref, z_ref = oracle.quantize_rows(ref, 8)
+        d = np.abs(codes.cpu().numpy().astype(int) - c_ref.astype(int))
+        nd = int((d > 0).sum())
+        lines.append(f"case {i:2d} {pro:11s} {str(dtype)[6:]:8s} M={M:5d} K={K:5d} "
+                     f"diff={nd} rate={nd / d.size:.2e}")
+        assert d.max() <= 1, lines[-1]
+        assert nd <= max(1e-4 * d.size, 1), lines[-1]
+        # the per-token scale is the reference's fp64 s of the row's fp32 range
+        assert np.allclose(s.cpu().numpy(), s_ref, rtol=1e-5, atol=0), lines[-1]
+        nd_all += nd
+        n_all += d.size
+    print("\n".join(lines))
+    print(f"pooled fast-mode code mismatch rate {nd_all / n_all:.2e} ({nd_all} of {n_all})")
+    assert nd_all <= 1e-4 * n_all

@@ -253,27 +253,36 @@ def test_prologue_modulate_exact(oracle):
     assert np.array_equal(codes.cpu().numpy(), c_ref) and np.array_equal(s.cpu().numpy(), s_ref)
     codes, s, z = dtq.quantize_rows(cuda(x), mode=dtq.MODE_FAST, prologue=pro)
     d = np.abs(codes.cpu().numpy().astype(int) - c_ref.astype(int))
-    assert d.max() <= 1 and (d > 0).mean() <= 1e-3
+    print(f"fast modulate: {(d > 0).mean():.2e} of codes differ")
+    assert d.max() <= 1 and (d > 0).mean() <= 1e-4
 
 
 @pytest.mark.parametrize("K", [1152, 1408, 3456, 4608])  # odd block counts: idle items
-def test_prologue_gelu_and_layernorm_run(K):
-    # GELU follows toydit.cpp:83; LayerNorm has no reference oracle (unpinned):
-    # compare with a torch fp64 restatement by tolerance only
+def test_prologue_gelu_and_layernorm_codes(oracle, K):
+    # GELU follows toydit.cpp:83 (the oracle's exact-erf gelu); LayerNorm has
+    # no reference oracle (parity unpinned), so its chain is an fp64
+    # restatement (biased variance, eps inside the sqrt).  Fast-mode codes
+    # against the fp64 chain: within 1 LSB on at most 1e-4 of codes, the
+    # north_star bar for fp32 transforms.
     rng = np.random.default_rng(9)
-    x = activations(rng, 128, K).astype(np.float32)
+    x = activations(rng, 512, K).astype(np.float32)
     xt = cuda(x)
-    xd = torch.from_numpy(x).double()
-    g = 0.5 * xd * (1 + torch.erf(xd / 2 ** 0.5))
+    xd = f64(x)
     codes, s, z = dtq.quantize_rows(xt, prologue=dtq.Prologue(dtq.PROLOGUE_GELU))
-    deq = (codes.double().cpu() - z.cpu()[:, None].double()) * s.cpu()[:, None]
-    assert (deq - g).abs().max() <= s.cpu().max() * 0.51 + 1e-4
-    sc = torch.zeros(K, device=DEV)
-    pro = dtq.Prologue(dtq.PROLOGUE_LN_MODULATE, sc, sc, 1e-6)
+    c_ref, s_ref, z_ref = oracle.quantize_rows(oracle.gelu(xd), 8)
+    d = np.abs(codes.cpu().numpy().astype(int) - c_ref.astype(int))
+    print(f"GELU K={K}: {(d > 0).mean():.2e} of codes differ")
+    assert d.max() <= 1 and (d > 0).mean() <= 1e-4
+    sc = (rng.standard_normal(K) * 0.2).astype(np.float32)
+    sh = (rng.standard_normal(K) * 0.1).astype(np.float32)
+    pro = dtq.Prologue(dtq.PROLOGUE_LN_MODULATE, cuda(sc), cuda(sh), 1e-6)
     codes, s, z = dtq.quantize_rows(xt, prologue=pro)
-    ln = (xd - xd.mean(1, keepdim=True)) / torch.sqrt(xd.var(1, unbiased=False, keepdim=True) + 1e-6)
-    deq = (codes.double().cpu() - z.cpu()[:, None].double()) * s.cpu()[:, None]
-    assert (deq - ln).abs().max() <= s.cpu().max() * 0.51 + 1e-3
+    mu = xd.mean(1, keepdims=True)
+    ln = (xd - mu) / np.sqrt(((xd - mu) ** 2).mean(1, keepdims=True) + 1e-6)
+    c_ref, s_ref, z_ref = oracle.quantize_rows(oracle.modulate(ln, f64(sc), f64(sh)), 8)
+    d = np.abs(codes.cpu().numpy().astype(int) - c_ref.astype(int))
+    print(f"LN-modulate K={K}: {(d > 0).mean():.2e} of codes differ")
+    assert d.max() <= 1 and (d > 0).mean() <= 1e-4
 
 
 def test_overflow_guard_and_shape_errors():

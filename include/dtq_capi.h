@@ -166,8 +166,12 @@ int dtq_qgemm(const uint8_t* codes, int64_t ldc, const double* s_x, const int32_
 /* ---------------------------------------------------------------- fused layer
  * Whole Matrix qlinear_forward(x, layer) (qgemm.cpp:23-67) on the device:
  * fused quantizer (prologue + the handle's balance) then the GEMM.
- * `workspace` [dev] of dtq_qlinear_workspace_bytes(h, M) bytes (codes and
- * per-token params), or NULL to use a handle-owned buffer.  Calls that use
+ * `workspace` [dev] of dtq_qlinear_workspace_bytes(h, M) bytes (row-flag
+ * counters, codes and per-token params), or NULL to use a handle-owned
+ * buffer.  A caller workspace must be zero-filled before its first use (its
+ * first 33 KB are the counters through which the GEMM consumes row blocks as
+ * the concurrently running quantizer publishes them); every forward leaves
+ * them zero again.  Calls that use
  * handle-owned scratch (workspace NULL, or y_dtype DTQ_F64, whose s32
  * accumulator is handle-owned) must be ordered on one stream or serialised
  * by the caller; with a caller workspace and a non-F64 output, calls on one

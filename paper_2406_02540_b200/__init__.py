@@ -42,6 +42,7 @@ EXPORTED = (
     "dtq_quantize_static", "dtq_dequantize", "dtq_balance_apply", "dtq_matmul_nt_f64",
     "dtq_checkpoint_open", "dtq_checkpoint_close", "dtq_checkpoint_num_layers",
     "dtq_checkpoint_layer_info", "dtq_checkpoint_load_layer",
+    "dtq_planned_create", "dtq_planned_destroy", "dtq_planned_select", "dtq_planned_bits",
 )
 
 
@@ -89,6 +90,10 @@ def lib():
     L.dtq_checkpoint_num_layers.argtypes = [p, p]
     L.dtq_checkpoint_layer_info.argtypes = [p, i64, p, p, p, p, p, p, p]
     L.dtq_checkpoint_load_layer.argtypes = [p, i64, i32, i32, p, p]
+    L.dtq_planned_create.argtypes = [p, i32, i64, i64, i64, p, i32, p, p, p, p]
+    L.dtq_planned_destroy.argtypes = [p]
+    L.dtq_planned_select.argtypes = [p, i64, i64, p]
+    L.dtq_planned_bits.argtypes = [p, i32, p]
     _lib = L
     return L
 
@@ -203,11 +208,13 @@ def quantize_rows(x, bits: int = 8, symmetric: bool = False, mode: int = MODE_FA
 class QuantLinear:
     """Device-resident QuantLinear (qgemm.hpp:17-24) behind an opaque handle."""
 
-    def __init__(self, handle: int, N: int, K: int, wbits: int, abits: int, balance=None):
+    def __init__(self, handle: int, N: int, K: int, wbits: int, abits: int, balance=None,
+                 owner=None):
         self._h = C.c_void_p(handle)
         self.N, self.K, self.weight_bits, self.act_bits = N, K, wbits, abits
         self.balance = balance
         self._ws = None
+        self._owner = owner  # a borrowed handle (PlannedLinear.select) is not destroyed here
 
     @classmethod
     def create(cls, w, weight_bits: int = 8, act_bits: int = 8, bias=None,
@@ -242,7 +249,7 @@ class QuantLinear:
         return cls(h.value, N, K, weight_bits, act_bits, balance)
 
     def close(self):
-        if self._h is not None and self._h.value:
+        if self._h is not None and self._h.value and self._owner is None:
             lib().dtq_qlinear_destroy(self._h)
         self._h = None
 
@@ -263,9 +270,11 @@ class QuantLinear:
         return codes, scale, wsum
 
     def workspace(self, M: int, device=None):
+        """A forward workspace for up to M rows (zeroed: its row-flag
+        counters must start at zero; every forward leaves them zero)."""
         torch = _torch()
         n = lib().dtq_qlinear_workspace_bytes(self._h, M)
-        return torch.empty(n, dtype=torch.uint8, device=device or "cuda")
+        return torch.zeros(n, dtype=torch.uint8, device=device or "cuda")
 
     def gemm(self, codes, s_x, z_x, out_dtype=None, out=None, stream=None):
         """Integer GEMM + epilogue on quantized activations (qgemm.cpp:52-63)."""
@@ -339,6 +348,79 @@ class QuantLinear:
                                               self._h, mode, y_host.data_ptr(),
                                               _dtype_code(y_host.dtype), _stream(stream)))
         return y_host
+
+
+NUM_RANGES = 4  # plan.hpp:17 kNumRanges
+
+
+def range_index(t: int, steps: int) -> int:
+    """Timestep range of denoising step t of `steps` (toydit.cpp:115)."""
+    if steps <= 0 or not 0 <= t < steps:
+        raise ValueError(f"step {t} outside [0, {steps})")
+    return t * NUM_RANGES // steps
+
+
+@dataclass
+class MixedPrecisionPlan:
+    """MixedPrecisionPlan (plan.hpp:30-40): weight bits per (layer, range)."""
+    bits: dict
+    budget: float = 8.0
+
+    def bits_for(self, layer: str, range_idx: int) -> int:
+        if layer not in self.bits:
+            raise ValueError(f"MixedPrecisionPlan: unknown layer {layer}")
+        row = self.bits[layer]
+        if not 0 <= range_idx < NUM_RANGES:
+            raise IndexError("MixedPrecisionPlan: range index out of range")  # array::at
+        return int(row[range_idx])
+
+
+class PlannedLinear:
+    """One layer of a MixedPrecisionPlan on the device (dtq_planned_*): a
+    device-resident QuantLinear per distinct weight width of the layer's
+    row, and the per-step dispatch of toydit.cpp:113-117."""
+
+    def __init__(self, handle: int, name: str, N: int, K: int, bits, act_bits: int):
+        self._h = C.c_void_p(handle)
+        self.name, self.N, self.K, self.bits, self.act_bits = name, N, K, tuple(bits), act_bits
+
+    @classmethod
+    def create(cls, w, plan: MixedPrecisionPlan, name: str, act_bits: int = 8, bias=None,
+               balance: Optional[Balance] = None, stream=None) -> "PlannedLinear":
+        torch = _torch()
+        _check_rows(w, w.shape[1] if w.dim() == 2 else -1, "planned weights")
+        N, K = w.shape
+        bits = [plan.bits_for(name, r) for r in range(NUM_RANGES)]
+        arr = (C.c_int32 * NUM_RANGES)(*bits)
+        bias_t = None if bias is None else torch.as_tensor(bias, dtype=torch.float64,
+                                                           device=w.device).contiguous()
+        h = C.c_void_p()
+        b = balance._c() if balance is not None else None
+        _check(lib().dtq_planned_create(w.data_ptr(), _dtype_code(w.dtype), N, K, w.stride(0), arr,
+                                        act_bits, _ptr(bias_t), _ref_or_none(b), _stream(stream),
+                                        C.byref(h)))
+        return cls(h.value, name, N, K, bits, act_bits)
+
+    def select(self, t: int, steps: int) -> QuantLinear:
+        """The QuantLinear serving step t of `steps` (borrowed from this layer)."""
+        h = C.c_void_p()
+        _check(lib().dtq_planned_select(self._h, t, steps, C.byref(h)))
+        return QuantLinear(h.value, self.N, self.K, self.bits[range_index(t, steps)],
+                           self.act_bits, owner=self)
+
+    def forward(self, x, t: int, steps: int, **kw):
+        return self.select(t, steps).forward(x, **kw)
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib().dtq_planned_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Checkpoint:

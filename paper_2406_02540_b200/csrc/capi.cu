@@ -135,6 +135,9 @@ int make_tmap_u8(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, i
   return DTQ_OK;
 }
 
+// row flags: 128-row blocks a forward can publish (M <= 1M rows)
+constexpr int kMaxFlagBlocks = 8192;
+
 // rotation blocks: the fused quantizers take up to 256 columns; wider blocks
 // (up to a full 16384-point rotation) take the fp64 pre-pass
 constexpr int kMaxFusedHblock = 256;
@@ -214,7 +217,9 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
                        const float* col_mul, const int8_t* signs, int hblock,
                        const dtq_prologue* pro, uint8_t* codes, int64_t ldc, double* scale,
                        int32_t* zero, int32_t* status, cudaStream_t st,
-                       bool col_mul_const = true) {
+                       bool col_mul_const = true, uint32_t* ready = nullptr,
+                       int partner_regs = 0, int partner_smem = 0, int* flags_used = nullptr) {
+  if (flags_used) *flags_used = 0;
   if (rows <= 0 || cols <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: empty matrix");
   if (!bits_supported(bits))
     return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: bits must be one of {2,4,6,8}");
@@ -360,9 +365,16 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
     const bool exact_v = kind == DTQ_PROLOGUE_NONE && !has_a && signs == nullptr;
     const int R = dtq_fq_tile_rows(rows, cols, static_cast<int>(es), has_a, has_b, kind, exact_v,
                                    sms);
-    if (R > 0)
+    if (R > 0) {
+      // row flags: the launcher keeps them only if the quantizer fits beside
+      // the GEMM on every SM (and says so in *flags_used)
+      a.ready = ready;
+      a.partner_regs = partner_regs;
+      a.partner_smem = partner_smem;
+      a.flags_used = flags_used;
       return fq_error(dtq_launch_fq_tile(a, static_cast<int>(es), x_dtype == DTQ_BF16 ? 1 : 0,
                                          signs != nullptr, R, sms, st));
+    }
   }
   // fast: G 8-lane groups per row, R = 4/G rows per warp with R*K <= 4608
   // (18 KB fp32 park buffer per warp); warps per CTA sized for ~2 CTAs/SM
@@ -538,13 +550,17 @@ struct dtq_qlinear_s {
 
 namespace {
 
-int grow(void** p, size_t* cur, size_t need) {
+// (zero_on: a forward workspace -- its row-flag counters must start at zero;
+// zeroed stream-ordered on that stream)
+int grow(void** p, size_t* cur, size_t need, cudaStream_t zero_on = nullptr,
+         bool zero = false) {
   if (*cur >= need) return DTQ_OK;
   if (*p) cudaFree(*p);
   *p = nullptr;
   *cur = 0;
   CUDA_TRY(cudaMalloc(p, need));
   *cur = need;
+  if (zero) CUDA_TRY(cudaMemsetAsync(*p, 0, need, zero_on));
   return DTQ_OK;
 }
 
@@ -745,7 +761,8 @@ unsigned long long* probe_buffer() {
 }
 
 int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32_t* z_x,
-               int64_t M, dtq_qlinear_s* h, void* y, int y_dtype, int64_t ldy, cudaStream_t st) {
+               int64_t M, dtq_qlinear_s* h, void* y, int y_dtype, int64_t ldy, cudaStream_t st,
+               uint32_t* ready = nullptr) {
   if (!h) return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: null handle");
   if (M <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: M must be >= 1");
   if (!codes || !s_x || !z_x || !y) return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: null pointer");
@@ -813,6 +830,10 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
   g.probe = probe_buffer();
   g.w4 = h->w4;
   g.ld4 = h->ld4;
+  // row flags (forward_impl, when the tile quantizer runs beside this GEMM)
+  g.ready = ready;
+  g.done = ready ? ready + kMaxFlagBlocks : nullptr;
+  g.mblocks = static_cast<int>((M + 127) / 128);
   static const bool no_tma_store = [] {
     const char* e = std::getenv("DTQ_DEBUG_NO_TMA_STORE");
     return e && e[0] == '1';
@@ -825,8 +846,9 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
     DTQ_TRY(cached_tmap_u8(h, &tY, yk, M, h->N * static_cast<int64_t>(es), ldk * es, 64, 32,
                            CU_TENSOR_MAP_SWIZZLE_64B));
 
-  const cudaError_t e = h->wbits != 4 ? dtq_launch_gemm_w8(tA, tB, tY, g, cfg, sms, st)
-                                      : dtq_launch_gemm_w4(tA, tB, tY, g, cfg, sms, st);
+  const cudaError_t e = ready ? dtq_launch_gemm_w8_cores(tA, tB, tY, g, cfg, sms, st)
+                       : h->wbits != 4 ? dtq_launch_gemm_w8(tA, tB, tY, g, cfg, sms, st)
+                                       : dtq_launch_gemm_w4(tA, tB, tY, g, cfg, sms, st);
   if (e != cudaSuccess) return fail(DTQ_ERR_CUDA, "qgemm launch: %s", cudaGetErrorString(e));
 
   if (y_dtype == DTQ_F64) {
@@ -839,12 +861,39 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
   return DTQ_OK;
 }
 
-size_t ws_layout(const dtq_qlinear_s* h, int64_t M, int64_t* ldc, size_t* off_s, size_t* off_z) {
+// workspace: [row-flag counters: kMaxFlagBlocks + the GEMM's exit ticket]
+// [codes M x ldc][s_x f64 M][z_x i32 M].  The counter region has a fixed size
+// (a workspace serves forwards of any M) and must be zero before first use;
+// every forward leaves it zero.
+constexpr size_t kFlagBytes = (kMaxFlagBlocks + 64) * sizeof(uint32_t);
+size_t ws_layout(const dtq_qlinear_s* h, int64_t M, int64_t* ldc, size_t* off_codes,
+                 size_t* off_s, size_t* off_z) {
   *ldc = round_up(h->K, 16);
-  const size_t codes = round_up(static_cast<int64_t>(M) * *ldc, 256);
+  *off_codes = kFlagBytes;
+  const size_t codes = kFlagBytes + round_up(static_cast<int64_t>(M) * *ldc, 256);
   *off_s = codes;
   *off_z = codes + round_up(M * 8, 256);
   return *off_z + round_up(M * 4, 256);
+}
+
+// Row flags for this forward?  The quantizer and the GEMM then run
+// concurrently, one CTA of each per SM (W8A8 with an fp32 epilogue output;
+// the tile quantizer; both fitting an SM -- checked by the launcher).
+// Opt-in (DTQ_ROW_FLAGS=1): measured SLOWER than the two stages back to back
+// on the C2 step (35.3 vs 28.3 us per forward in a CUDA graph,
+// profiles/r02_rowflags.md).  Programmatic launch does co-schedule the GEMM
+// beside the quantizer, but each forward's quantizer still waits for the
+// whole previous GEMM (its input may be that GEMM's output), the GEMM's CTAs
+// need the SM space the previous GEMM's tail CTAs hold, and the quantizer at
+// one CTA per SM is ~1.4x slower -- the overlap it buys is smaller than what
+// it costs.  Kept, tested (tests/test_gpu_rowflags.py), off by default.
+bool row_flags_wanted(const dtq_qlinear_s* h, int64_t M, int y_dtype) {
+  static const bool on = [] {
+    const char* e = std::getenv("DTQ_ROW_FLAGS");
+    return e != nullptr && e[0] == '1';
+  }();
+  return on && h->wbits != 4 && (M + 127) / 128 <= kMaxFlagBlocks &&
+         (y_dtype == DTQ_F16 || y_dtype == DTQ_BF16 || y_dtype == DTQ_F32);
 }
 
 int forward_impl(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear_s* h, int mode,
@@ -853,24 +902,35 @@ int forward_impl(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear
   if (!h) return fail(DTQ_ERR_INVALID_ARGUMENT, "forward: null handle");
   if (ldx < h->K) return fail(DTQ_ERR_INVALID_ARGUMENT, "qlinear_forward: X cols != C_in");
   int64_t ldc;
-  size_t off_s, off_z;
-  const size_t need = ws_layout(h, M, &ldc, &off_s, &off_z);
+  size_t off_c, off_s, off_z;
+  const size_t need = ws_layout(h, M, &ldc, &off_c, &off_s, &off_z);
   if (!ws) {
-    DTQ_TRY(grow(&h->scratch, &h->scratch_bytes, need));
+    DTQ_TRY(grow(&h->scratch, &h->scratch_bytes, need, st, true));
     ws = h->scratch;
   } else if (ws_bytes < need) {
     return fail(DTQ_ERR_INVALID_ARGUMENT, "forward: workspace too small (%zu < %zu)", ws_bytes,
                 need);
   }
   uint8_t* base = static_cast<uint8_t*>(ws);
-  uint8_t* codes = base;
+  uint32_t* ready = reinterpret_cast<uint32_t*>(base);
+  uint8_t* codes = base + off_c;
   double* s_x = reinterpret_cast<double*>(base + off_s);
   int32_t* z_x = reinterpret_cast<int32_t*>(base + off_z);
   DTQ_TRY(overflow_check(h->abits, h->wbits, h->K));
+  int p_regs = 0, p_smem = 0, flags = 0;
+  if (row_flags_wanted(h, M, y_dtype)) {
+    DTQ_TRY(check_device());
+    const GemmCfg cfg = choose_gemm_cfg(M, h->N, h->wbits, device_info().sms);
+    const int kind = y_dtype == DTQ_F16 ? dtq_gemm::kOutF16
+                     : y_dtype == DTQ_BF16 ? dtq_gemm::kOutBF16 : dtq_gemm::kOutF32;
+    if (dtq_gemm_w8_cores_info(cfg, kind, &p_regs, &p_smem) != 0) ready = nullptr;
+  } else {
+    ready = nullptr;
+  }
   DTQ_TRY(quantize_rows_impl(x, x_dtype, M, h->K, ldx, h->abits, 0, mode, 0, h->smooth,
                              h->col_mul, h->signs, h->hblock, pro, codes, ldc, s_x, z_x,
-                             status, st));
-  return qgemm_impl(codes, ldc, s_x, z_x, M, h, y, y_dtype, ldy, st);
+                             status, st, true, ready, p_regs, p_smem, &flags));
+  return qgemm_impl(codes, ldc, s_x, z_x, M, h, y, y_dtype, ldy, st, flags ? ready : nullptr);
 }
 
 }  // namespace
@@ -1185,8 +1245,8 @@ int dtq_qgemm(const uint8_t* codes, int64_t ldc, const double* s_x, const int32_
 size_t dtq_qlinear_workspace_bytes(dtq_qlinear_t h, int64_t M) {
   if (!h || M <= 0) return 0;
   int64_t ldc;
-  size_t a, b;
-  return ws_layout(h, M, &ldc, &a, &b);
+  size_t a, b, c;
+  return ws_layout(h, M, &ldc, &a, &b, &c);
 }
 
 int dtq_qlinear_forward(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear_t h,
@@ -1239,9 +1299,9 @@ int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_
     CUDA_TRY(cudaMemcpyAsync(y, h->hy, yb, cudaMemcpyDeviceToHost, st));
   } else {
     int64_t ldc;
-    size_t a_, b_;
-    const size_t wsb = ws_layout(h, chunk, &ldc, &a_, &b_);
-    DTQ_TRY(grow(&h->pws, &h->pws_bytes, wsb));
+    size_t a_, b_, c_;
+    const size_t wsb = ws_layout(h, chunk, &ldc, &a_, &b_, &c_);
+    DTQ_TRY(grow(&h->pws, &h->pws_bytes, wsb, st, true));
     for (cudaStream_t& s : h->ps)
       if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     for (cudaEvent_t& e : h->pe)

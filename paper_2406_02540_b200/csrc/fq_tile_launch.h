@@ -32,6 +32,12 @@ inline cudaError_t fq_tile_occupancy(const void* kern, int block, size_t smem, i
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
     if (e != cudaSuccess) return e;
+    // the whole unified L1 / shared array as shared memory: an SM running
+    // this kernel can then also host the co-resident GEMM CTA (the carveout
+    // is fixed while any CTA is resident on the SM)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
     mx = smem;
   }
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, block, smem);
@@ -40,8 +46,23 @@ inline cudaError_t fq_tile_occupancy(const void* kern, int block, size_t smem, i
   return cudaSuccess;
 }
 
+// Registers per thread of a kernel (cached; cudaFuncGetAttributes costs
+// host microseconds)
+inline int fq_kernel_regs(const void* kern) {
+  static std::mutex mu;
+  static std::map<const void*, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto it = cache.find(kern);
+  if (it != cache.end()) return it->second;
+  cudaFuncAttributes at{};
+  const int r = cudaFuncGetAttributes(&at, kern) == cudaSuccess ? at.numRegs : 255;
+  cache[kern] = r;
+  return r;
+}
+
 template <typename Tin, bool kRot, bool kExactV, int kPro>
-cudaError_t launch_tile(const dtq_fq::FqArgs& a, int R, int nbuf, int sms, cudaStream_t st) {
+cudaError_t launch_tile(const dtq_fq::FqArgs& a_in, int R, int nbuf, int sms, cudaStream_t st) {
+  dtq_fq::FqArgs a = a_in;
   // K <= 1152: 4 lanes per block, 8-row tiles (288 threads); wider: 2 lanes
   // per block, 8 or 4 rows (576 threads)
   const bool wide = dtq_fq::fq_lanes(a.K, a.pro) == 2;
@@ -61,6 +82,23 @@ cudaError_t launch_tile(const dtq_fq::FqArgs& a, int R, int nbuf, int sms, cudaS
     return e ? std::atoi(e) : 0;
   }();
   if (occ_cap > 0 && occ > occ_cap) occ = occ_cap;
+  if (a.ready != nullptr) {
+    // row flags: one quantizer CTA per SM next to one GEMM CTA, which runs
+    // concurrently and consumes the rows as they are published.  Both must
+    // fit an SM together (64K registers in 256-register warp granules; 228 KB
+    // of shared memory with 1 KB reserved per CTA, 1 KB of static smem here;
+    // partner_smem includes the GEMM's reserved KB), else no flags.
+    const int regs = (fq_kernel_regs(reinterpret_cast<const void*>(kern)) + 7) / 8 * 8;
+    const int64_t fq_regs = static_cast<int64_t>(regs) * ((block + 31) / 32 * 32);
+    const bool fits = fq_regs + a.partner_regs <= 65536 &&
+                      static_cast<int64_t>(L.bytes) + 2048 + a.partner_smem <= 228 * 1024;
+    if (fits) {
+      occ = 1;
+    } else {
+      a.ready = nullptr;
+    }
+  }
+  if (a.flags_used) *a.flags_used = a.ready != nullptr ? 1 : 0;
   const int64_t cap = static_cast<int64_t>(sms) * (occ > 0 ? occ : 1);
   const int grid = static_cast<int>(tiles < cap ? tiles : cap);
   // programmatic dependent launch: the CTAs' setup (barriers, the per-column

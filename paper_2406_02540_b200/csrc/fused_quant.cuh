@@ -62,6 +62,14 @@ struct FqArgs {
   const float* col_mul;       // fast kernel: folded sign/s_c/sqrt(hblock) per column
   int col_mul_const;          // 1: col_mul is a layer constant (written before the
                               // producer of X ran), readable before griddepcontrol.wait
+  uint32_t* ready;            // tile kernel: per-128-row-block rows-ready counters the
+                              // concurrently running GEMM waits on (nullptr: none)
+  // host side (launcher only): the co-resident GEMM's per-SM registers and
+  // shared memory; the launcher keeps `ready` only if one quantizer CTA fits
+  // beside it on every SM, and reports that in *flags_used
+  int partner_regs;
+  int partner_smem;
+  int* flags_used;
   unsigned long long* probe;  // diagnostics: per-warp phase cycles (or nullptr)
   int tpr;                    // threads per row (multiple of 16 and of hblock/8)
   int dbg;                    // diagnostics (tile kernel): 1 = skip the transform

@@ -247,6 +247,15 @@ __device__ __forceinline__ void fq_tile_codes(const float2 (&P)[FqShape<kQ>::kPa
 #define FQ_DBG(a) 0
 #endif
 
+// Rows [tile * R, +R) are stored: add them to their 128-row block's counter
+// (release at gpu scope, after the CTA barrier that ordered every thread's
+// stores).  The GEMM's producer waits for min(128, M - 128 b) rows.
+__device__ __forceinline__ void fq_publish_rows(const FqArgs& a, int64_t tile, int R) {
+  const int64_t row0 = tile * R;
+  const int64_t n = a.M - row0 < R ? a.M - row0 : R;
+  dtq_ptx::red_release_add(a.ready + (row0 >> 7), static_cast<uint32_t>(n));
+}
+
 template <typename Tin, bool kRot, bool kExactV, int kPro, bool kWide, int kR>
 __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
     fq_tile_kernel(const FqArgs a) {
@@ -298,7 +307,9 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
 #ifdef FQ_TILE_PROBE
   const unsigned long long pr_g0 = dtq_ptx::globaltimer_ns();
 #endif
-  dtq_ptx::pdl_launch_dependents();  // let the GEMM that consumes the codes launch early
+  // Without row flags the GEMM may launch at once: its prologue (TMEM, barriers,
+  // descriptors) overlaps this kernel, and it waits for the whole grid.
+  if (a.ready == nullptr) dtq_ptx::pdl_launch_dependents();
   // warp 0: barriers, then the first tile's copies (overlap the table setup).
   // Under programmatic dependent launch everything before pdl_wait() runs
   // while the kernel producing X drains: only layer constants are read there.
@@ -326,6 +337,11 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
     }
   }
   dtq_ptx::pdl_wait();  // X (and the modulate vectors) come from earlier kernels
+  // With row flags the GEMM may launch only now: it reads rows as they are
+  // published, so it must never run while the kernel before this one (the
+  // previous layer's GEMM) still does -- the row counters and the workspace
+  // are then never shared between two forwards in flight.
+  if (a.ready != nullptr) dtq_ptx::pdl_launch_dependents();
   if (warp == 0) {  // the ring's first nbuf - 1 tiles
     __syncwarp();
     for (int k = 0; k + 1 < nbuf; ++k)
@@ -634,6 +650,9 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
       __syncthreads();  // the one barrier per tile (also frees the input buffer)
       if (probe) pr_bar += clock64() - b0;
     }
+    // every thread's code / param stores of the previous tile precede this
+    // barrier: publish those rows to the GEMM waiting on their block
+    if (a.ready != nullptr && t == 0 && it > 0) fq_publish_rows(a, tile - gridDim.x, R);
     if (!ok) continue;
     float mn = __int_as_float(0x7f800000), mx = -mn;
     const int nwarp = (nb * R + kFqItems - 1) / kFqItems;  // one partial per warp
@@ -708,6 +727,13 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
       fq_tile_codes<kFqQ, true, kExactV>(P, inv_sf, zm, qmax_i, num, den, z, qmax, dst);
     else
       fq_tile_codes<kFqQ, false, kExactV>(P, inv_sf, zm, qmax_i, num, den, z, qmax, dst);
+    // the GEMM reads these codes through TMA (async proxy)
+    if (a.ready != nullptr) dtq_ptx::fence_proxy_async_global();
+  }
+  if (a.ready != nullptr) {  // publish the CTA's last tile
+    __syncthreads();
+    const int64_t nt = (a.M + R - 1) / R;
+    if (t == 0 && blockIdx.x < nt) fq_publish_rows(a, tile - gridDim.x, R);
   }
 #ifdef FQ_TILE_PROBE
   if (probe) {

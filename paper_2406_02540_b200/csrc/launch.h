@@ -37,18 +37,29 @@ cudaError_t dtq_launch_gemm_w4(const CUtensorMap& tA, const CUtensorMap& tB,
                                const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, GemmCfg c,
                                int sms, cudaStream_t st);
 
-template <int BN, int kStages, bool kW4, int kOut, bool k2Cta>
+// W8A8 tiles that share each SM with the tile quantizer (row flags):
+// per-SM registers / shared memory of the instance for (c, out_kind), and the
+// launcher (gemm_w8_cores.cu)
+int dtq_gemm_w8_cores_info(GemmCfg c, int out_kind, int* regs_per_sm, int* smem);
+cudaError_t dtq_launch_gemm_w8_cores(const CUtensorMap& tA, const CUtensorMap& tB,
+                                     const CUtensorMap& tY, const dtq_gemm::GemmArgs& g,
+                                     GemmCfg c, int sms, cudaStream_t st);
+
+template <int BN, int kStages, bool kW4, int kOut, bool k2Cta, bool kCoRes = false>
 cudaError_t dtq_launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB,
                               const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, int sms,
                               cudaStream_t st) {
   using L = dtq_gemm::Smem<BN, kStages, kW4, k2Cta>;
-  auto kern = dtq_gemm::qgemm_kernel<BN, kStages, kW4, kOut, k2Cta>;
+  auto kern = dtq_gemm::qgemm_kernel<BN, kStages, kW4, kOut, k2Cta, kCoRes>;
   static thread_local int configured_dev = -1;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (configured_dev != dev) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::alloc);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
     configured_dev = dev;
   }

@@ -86,6 +86,35 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ---------------------------------------------------------------- cross-kernel row flags
+// Per-128-row-block "rows ready" counters between a producer kernel that
+// writes rows with generic stores (the fused quantizer) and a consumer kernel
+// running concurrently that reads them through TMA (the GEMM's async proxy).
+// Producer: every writer thread fence.proxy.async.global after its stores,
+// CTA barrier, then one thread red.release.gpu.add; consumer: ld.acquire.gpu
+// spin, then fence.proxy.async.global before its TMA loads.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin until *p >= want (acquire), with a backoff and the same ~10 s
+// watchdog as mbar_wait: a protocol bug traps instead of hanging the GPU.
+__device__ __forceinline__ void wait_rows_ready(const uint32_t* p, uint32_t want) {
+  if (ld_acquire_u32(p) >= want) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_u32(p) < want) {
+    __nanosleep(64);
+    if (globaltimer_ns() - t0 > 10000000000ull) __trap();
+  }
+}
+
 // ---------------------------------------------------------------- clusters
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

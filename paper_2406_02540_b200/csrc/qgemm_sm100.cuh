@@ -56,6 +56,15 @@ struct GemmArgs {
                         // 3 loads + dequant math, 4 + smem staging (no stores)
   const uint8_t* w4;    // W4A8 single-CTA tiles: packed nibbles [N, ld4] (read by the
   int64_t ld4;          // converter warps straight from L2)
+  // Row flags (forward with the tile quantizer running concurrently): per
+  // 128-row block, the number of rows whose codes / s_x / z_x are stored.
+  // nullptr: the codes are complete before the kernel starts (griddepcontrol
+  // .wait).  With flags, tiles run n-fastest (early row blocks first), the
+  // producer and the epilogue wait on their block, and the last CTA to exit
+  // resets the counters (and the `done` ticket) to zero for the next forward.
+  uint32_t* ready;
+  uint32_t* done;
+  int mblocks;          // ceil(M / 128): counters to reset
 };
 
 constexpr int BM = 128;
@@ -177,8 +186,14 @@ __device__ __forceinline__ uint2 w4_word_to_s8x8_x16(uint32_t w) {
 #define GEMM_PROBE(g) static_cast<unsigned long long*>(nullptr)
 #endif
 
-template <int BN, int kStages, bool kW4, int kOut, bool k2Cta>
-__global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
+#ifndef DTQ_CORES_MAXNREG
+#define DTQ_CORES_MAXNREG 112
+#endif
+// kCoRes: the instance shares every SM with a tile-quantizer CTA (row flags):
+// capped at 112 registers per thread so both CTAs' registers fit the SM (the
+// others at 200, what 320 threads of one CTA per SM allow anyway).
+template <int BN, int kStages, bool kW4, int kOut, bool k2Cta, bool kCoRes = false>
+__global__ void __launch_bounds__(num_threads<BN, kW4>(), 1) __maxnreg__(kCoRes ? DTQ_CORES_MAXNREG : 200)
     qgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmY, const GemmArgs g) {
   using namespace dtq_ptx;
@@ -228,8 +243,17 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
   };
   const int tile0 = k2Cta ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
   const int tstride = k2Cta ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  // tile -> (m, n): m fastest (B tiles stay in L2 across a wave), or n fastest
+  // with row flags (a wave needs only the first row blocks the quantizer
+  // publishes)
+  const bool flags = g.ready != nullptr;
+  auto tile_m = [&](int t) { return flags ? t / g.tiles_n : t % g.tiles_m; };
+  auto tile_n = [&](int t) { return flags ? t % g.tiles_n : t / g.tiles_m; };
+  // rows of 128-row block `mb` to wait for (0 past M: TMA zero-fills them)
+  auto block_rows = [&](int mb) { return g.M - mb * 128 < 128 ? g.M - mb * 128 : 128; };
 
   const long long t_start = clock64();
+  const unsigned long long g_start_ns = GEMM_PROBE(g) ? globaltimer_ns() : 0ull;
   if (warp == kTmaWarp && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
@@ -262,7 +286,9 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();  // A codes, s_x, z_x come from the preceding quantizer kernel
+  // A codes, s_x, z_x come from the preceding quantizer kernel: all of them
+  // at once (griddepcontrol.wait), or row block by row block (flags)
+  if (!flags) pdl_wait();
   pdl_launch_dependents();  // the next layer's quantizer may set up on freed SMs
 
   if (warp == kTmaWarp) {
@@ -271,8 +297,17 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       int s = 0;
       uint32_t ph = 0;
       for (int tile = tile0; tile < total_tiles; tile += tstride) {
-        const int m0 = (tile % g.tiles_m) * kTileM + rank * BM;
-        const int n0 = (tile / g.tiles_m) * BN;
+        const int m0 = tile_m(tile) * kTileM + rank * BM;
+        const int n0 = tile_n(tile) * BN;
+        if (flags) {
+          // this CTA's A rows (both sub-tiles with kM2) must be published
+#pragma unroll
+          for (int sub = 0; sub < (kM2 ? 2 : 1); ++sub) {
+            const int mb = (m0 >> 7) + sub;
+            if (mb * 128 < g.M) wait_rows_ready(g.ready + mb, static_cast<uint32_t>(block_rows(mb)));
+          }
+          fence_proxy_async_global();  // generic-proxy stores -> this thread's TMA reads
+        }
         for (int kb = 0; kb < g.k_blocks; ++kb) {
           timed_wait(&empty[s], ph ^ 1, pw0);
           if constexpr (k2Cta && kW4 && L::kP > 0) {
@@ -396,8 +431,8 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     double nsx = 0.0;
     int32_t nzx = 0;
     auto fetch = [&](int t) {
-      const int tm0 = (t % g.tiles_m) * kTileM + rank * BM;
-      const int tn0 = (t / g.tiles_m) * BN;
+      const int tm0 = tile_m(t) * kTileM + rank * BM;
+      const int tn0 = tile_n(t) * BN;
       p_ok = 0;
 #pragma unroll
       for (int i = 0; i < kParPer; ++i) {
@@ -411,15 +446,24 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
       }
       const int row = tm0 + qrow + lane;
       p_ok |= row < g.M ? (1u << 31) : 0u;
-      nsx = __ldg(g.s_x + min(row, g.M - 1));
-      nzx = __ldg(g.z_x + min(row, g.M - 1));
+      if (flags) {
+        // s_x / z_x of rows the quantizer is still writing: wait for the
+        // block, then read around L1 (no non-coherent __ldg)
+        const int mb = (tm0 + qrow) >> 7;
+        if (mb * 128 < g.M) wait_rows_ready(g.ready + mb, static_cast<uint32_t>(block_rows(mb)));
+        nsx = __ldcg(g.s_x + min(row, g.M - 1));
+        nzx = __ldcg(g.z_x + min(row, g.M - 1));
+      } else {
+        nsx = __ldg(g.s_x + min(row, g.M - 1));
+        nzx = __ldg(g.z_x + min(row, g.M - 1));
+      }
     };
     if (tile0 < total_tiles) fetch(tile0);
     for (int tile = tile0; tile < total_tiles; tile += tstride, ++it) {
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
-      const int m0 = (tile % g.tiles_m) * kTileM + rank * BM;
-      const int n0 = (tile / g.tiles_m) * BN;
+      const int m0 = tile_m(tile) * kTileM + rank * BM;
+      const int n0 = tile_n(tile) * BN;
       uint32_t* par = sPar + acc * (3 * BN);
 #pragma unroll
       for (int i = 0; i < kParPer; ++i) {
@@ -669,7 +713,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     const int ct = (cw % kGW) * 32 + static_cast<int>(lane);    // thread within the group
     constexpr int kIt = L::kBRows * 8 / (32 * kGW);
     auto load = [&](int t, int kb, uint2 (&v)[kIt]) {
-      const int n0 = (t / g.tiles_m) * BN + rank * L::kBRows;
+      const int n0 = tile_n(t) * BN + rank * L::kBRows;
 #pragma unroll
       for (int i = 0; i < kIt; ++i) {
         const int item = ct + i * 32 * kGW;
@@ -746,13 +790,30 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
     unsigned long long* pr = GEMM_PROBE(g) + blockIdx.x * 8;
     if (warp == kTmaWarp) pr[0] = pw0;
     if (warp == kMmaWarp) { pr[1] = pw0; pr[2] = pw1; }
-    if (warp == 0) { pr[3] = pw0; pr[4] = pw1; pr[5] = clock64() - t_start; }
+    if (warp == 0) {
+      pr[3] = pw0;
+      pr[4] = pw1;
+      pr[5] = clock64() - t_start;
+      pr[6] = g_start_ns;            // CTA start / end (globaltimer): timelines
+      pr[7] = globaltimer_ns();
+    }
   }
   tc_fence_before();
   if constexpr (k2Cta)
     cluster_sync();
   else
     __syncthreads();
+  if (flags && threadIdx.x == 0) {
+    // every row flag this CTA reads has been read: the last CTA out resets
+    // them for the next forward (which can only start its quantizer after
+    // this grid completes)
+    __threadfence();
+    if (atomicAdd(g.done, 1u) == gridDim.x - 1) {
+      for (int i = 0; i < g.mblocks; ++i) g.ready[i] = 0u;
+      *g.done = 0u;
+      __threadfence();
+    }
+  }
   if (warp == kMmaWarp) {
     tc_fence_after();
     if constexpr (k2Cta)

@@ -64,3 +64,27 @@ def test_hadamard_signs_match_the_oracle_engine(oracle):
     import numpy as np
     for seed, n in [(7, 1152), (0, 64), (123, 4608)]:
         assert np.array_equal(dtq.hadamard_signs(n, seed), oracle.hadamard_signs(n, seed))
+
+
+def test_mixed_precision_plan_mirror():
+    # plan.hpp:30-40 bits_for (unknown layer -> std::invalid_argument) and the
+    # range index of toydit.cpp:115 (t * 4 / steps)
+    plan = dtq.MixedPrecisionPlan({"attn.qkv": (8, 4, 4, 4), "mlp.fc1": (4, 4, 4, 8)}, 5.0)
+    assert plan.bits_for("attn.qkv", 0) == 8 and plan.bits_for("mlp.fc1", 3) == 8
+    with pytest.raises(ValueError, match="unknown layer"):
+        plan.bits_for("mlp.fc2", 0)
+    assert [dtq.range_index(t, 20) for t in (0, 4, 5, 9, 10, 14, 15, 19)] == \
+        [0, 0, 1, 1, 2, 2, 3, 3]
+    assert [dtq.range_index(t, 6) for t in range(6)] == [0, 0, 1, 2, 2, 3]
+    with pytest.raises(ValueError):
+        dtq.range_index(20, 20)
+
+
+def test_planned_layer_rejects_unquantized_widths_before_the_device():
+    if not os.path.exists(dtq.LIB_PATH):
+        pytest.skip("libdtq_b200.so not built")
+    L = dtq.lib()
+    h = ctypes.c_void_p()
+    bits = (ctypes.c_int32 * 4)(8, 16, 4, 4)  # 16 = the reference's FP passthrough
+    st = L.dtq_planned_create(1, dtq.F16, 4, 8, 8, bits, 8, None, None, None, ctypes.byref(h))
+    assert st == dtq.DTQ_ERR_INVALID_ARGUMENT and b"range 1" in L.dtq_last_error()

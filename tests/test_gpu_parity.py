@@ -518,3 +518,43 @@ def test_c5_full_size_balanced_row_shards(oracle, wb):
     assert np.array_equal(acc.cpu().numpy()[rows].astype(np.int64), acc_ref)
     y_ref = oracle.qlinear_epilogue(acc_ref, s.cpu().numpy()[rows], sw, bias)
     assert rel_err(y.float().cpu().numpy()[rows], y_ref) <= REL_TOL
+
+
+def test_planned_layer_dispatch_per_range():
+    # a22: the device dispatch of a MixedPrecisionPlan row (toydit.cpp:113-117):
+    # step t of `steps` runs bits_for(layer, t * 4 / steps); each range's
+    # output equals a layer built at that width alone, bit for bit
+    rng = np.random.default_rng(31)
+    K, N, M = 1152, 640, 300
+    w = cuda(rng.standard_normal((N, K)).astype(np.float16) / np.sqrt(K))
+    signs = cuda(dtq.hadamard_signs(K, 7))
+    bal = dtq.Balance(cuda(rng.uniform(0.5, 2.0, K)), signs, 128)
+    bias = cuda(rng.standard_normal(N) * 0.1)
+    plan = dtq.MixedPrecisionPlan({"blocks.0.mlp.fc1": (8, 4, 4, 6)})
+    pl = dtq.PlannedLinear.create(w, plan, "blocks.0.mlp.fc1", bias=bias, balance=bal)
+    x = cuda(activations(rng, M, K))
+    alone = {b: dtq.QuantLinear.create(w, b, 8, bias=bias, balance=bal) for b in (8, 4, 6)}
+    steps = 20
+    for t in range(steps):
+        b = plan.bits_for("blocks.0.mlp.fc1", dtq.range_index(t, steps))
+        layer = pl.select(t, steps)
+        assert layer.weight_bits == b
+        assert torch.equal(pl.forward(x, t, steps), alone[b].forward(x)), (t, b)
+    with pytest.raises(ValueError):
+        pl.select(steps, steps)
+
+
+def test_row_flag_path_subprocess():
+    # the opt-in concurrent quantizer -> GEMM path (row flags) must stay
+    # bit-identical to the two stages back to back: tests/test_gpu_rowflags.py
+    # in a process of its own with the switch on
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DTQ_ROW_FLAGS="1", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_rowflags.py")],
+                       capture_output=True, text=True, env=env, timeout=600, cwd=root)
+    print(r.stdout[-2000:])
+    assert r.returncode == 0 and " passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]

@@ -756,15 +756,17 @@ def rooflines(r):
             ceiling = tj.get("int8_ceiling_tops")
         except Exception:
             pass
-    roof = {"bound": "tensor", "achieved": gemm_tops, "peak": int8_peak, "unit": "TFLOP/s",
-            "frac": gemm_tops / int8_peak, "traffic": traffic,
+    # peak: the dense INT8 tensor ceiling measured on this pool's B200s
+    # (tools/int8_ceiling.cu: the GEMM's own tcgen05.mma.kind::i8 back to back
+    # from smem), else 2 x the driver-measured dense bf16
+    peak = float(ceiling) if ceiling else int8_peak
+    roof = {"bound": "tensor", "achieved": gemm_tops, "peak": peak, "unit": "TFLOP/s",
+            "frac": gemm_tops / peak, "traffic": traffic,
             "kernel": "qgemm_kernel (tcgen05.mma kind::i8)",
-            "peak_source": f"2 x {peak_src} dense bf16 ({bf16:.1f} TF/s); nominal int8 dense "
-                           "4500 TOPS",
-            "frac_of_nominal": gemm_tops / 4500.0, "algorithmic_bytes": gemm_bytes}
-    if ceiling:
-        roof["measured_int8_ceiling_tops"] = ceiling
-        roof["frac_of_measured_int8_ceiling"] = gemm_tops / ceiling
+            "peak_source": ("measured dense INT8 ceiling (profiles/r02_int8_ceiling.json)"
+                            if ceiling else f"2 x {peak_src} dense bf16 ({bf16:.1f} TF/s)"),
+            "frac_of_2x_measured_bf16": gemm_tops / int8_peak,
+            "frac_of_nominal_4500": gemm_tops / 4500.0, "algorithmic_bytes": gemm_bytes}
     fq = {"bound": "hbm", "achieved": fq_bytes / r["t_fq"] / 1e9, "peak": hbm, "unit": "GB/s",
           "frac": fq_bytes / r["t_fq"] / 1e9 / hbm, "ms": r["t_fq"] * 1e3, "bytes": fq_bytes,
           "peak_source": peak_src,

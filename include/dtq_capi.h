@@ -229,6 +229,18 @@ int dtq_balance_apply(const double* x, int64_t rows, int64_t cols, int64_t ldx,
 int dtq_matmul_nt_f64(const double* x, int64_t M, int64_t K, const double* w, int64_t N,
                       const double* bias, double* y, void* stream);
 
+/* Calibration statistics (matrix.hpp:95-109): out[c] = max_r |x[r,c]|
+ * (col, out [dev] cols) / out[r] = max_c |x[r,c]| (row, out [dev] rows). */
+int dtq_col_absmax_f64(const double* x, int64_t rows, int64_t cols, int64_t ldx, double* out,
+                       void* stream);
+int dtq_row_absmax_f64(const double* x, int64_t rows, int64_t cols, int64_t ldx, double* out,
+                       void* stream);
+
+/* fwht (balance.cpp:22-33) in place on each of `rows` rows of n values
+ * (n a power of two <= 16384): the unnormalised radix-2 butterflies in the
+ * reference's order, no signs, no 1/sqrt(n). */
+int dtq_fwht_f64(double* x, int64_t rows, int64_t n, int64_t ldx, void* stream);
+
 /* ---------------------------------------------------------------- checkpoints
  * read_checkpoint (trace_io.cpp:263-316) straight onto the device.  The
  * file is the reference's little-endian format: "DTQCKPT\0", u16 version 1,

@@ -43,6 +43,7 @@ EXPORTED = (
     "dtq_checkpoint_open", "dtq_checkpoint_close", "dtq_checkpoint_num_layers",
     "dtq_checkpoint_layer_info", "dtq_checkpoint_load_layer",
     "dtq_planned_create", "dtq_planned_destroy", "dtq_planned_select", "dtq_planned_bits",
+    "dtq_col_absmax_f64", "dtq_row_absmax_f64", "dtq_fwht_f64",
 )
 
 

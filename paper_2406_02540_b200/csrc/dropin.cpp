@@ -10,8 +10,10 @@
 // fallback) raises std::runtime_error.
 //
 // Host-side pieces are bookkeeping and analysis only: grouping indices,
-// round_even (the rounding definition), error_report / incoherence, the
-// calibration-time scaling mask and sign draw, byte accounting.
+// round_even (the rounding definition), error_report / incoherence / mse, the
+// calibration-time scaling mask and sign draw, byte accounting.  The
+// calibration statistics (col_absmax / row_absmax), fwht and choose_alpha's
+// matrices run on the device.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -294,17 +296,23 @@ double mse(const Matrix& a, const Matrix& b) {
   return acc / static_cast<double>(a.size());
 }
 
+// calibration statistics on the device (max is exact: any reduction order
+// gives the reference's values)
 std::vector<double> col_absmax(const Matrix& m) {
   std::vector<double> out(m.cols(), 0.0);
-  for (std::size_t r = 0; r < m.rows(); ++r)
-    for (std::size_t c = 0; c < m.cols(); ++c) out[c] = std::max(out[c], std::abs(m(r, c)));
+  if (m.rows() == 0 || m.cols() == 0) return out;
+  Dev<double> dx(m.data().data(), m.size()), dout(m.cols());
+  check(dtq_col_absmax_f64(dx.p, m.rows(), m.cols(), m.cols(), dout.p, nullptr));
+  dout.get(out.data());
   return out;
 }
 
 std::vector<double> row_absmax(const Matrix& m) {
   std::vector<double> out(m.rows(), 0.0);
-  for (std::size_t r = 0; r < m.rows(); ++r)
-    for (std::size_t c = 0; c < m.cols(); ++c) out[r] = std::max(out[r], std::abs(m(r, c)));
+  if (m.rows() == 0 || m.cols() == 0) return out;
+  Dev<double> dx(m.data().data(), m.size()), dout(m.rows());
+  check(dtq_row_absmax_f64(dx.p, m.rows(), m.cols(), m.cols(), dout.p, nullptr));
+  dout.get(out.data());
   return out;
 }
 
@@ -457,13 +465,13 @@ double incoherence(std::span<const double> group) {
 
 // ================================================================ balance.hpp
 void fwht(double* data, std::size_t n) {
-  for (std::size_t h = 1; h < n; h <<= 1)
-    for (std::size_t i = 0; i < n; i += 2 * h)
-      for (std::size_t j = i; j < i + h; ++j) {
-        const double a = data[j], b = data[j + h];
-        data[j] = a + b;
-        data[j + h] = a - b;
-      }
+  // on the device, the reference's butterfly order (balance.cpp:22-33); the
+  // reference's loop reads past the end for n that is not a power of two
+  if (n <= 1) return;
+  if ((n & (n - 1)) != 0) throw std::invalid_argument("fwht: n must be a power of two");
+  Dev<double> dx(data, n);
+  check(dtq_fwht_f64(dx.p, 1, static_cast<int64_t>(n), static_cast<int64_t>(n), nullptr));
+  dx.get(data);
 }
 
 ScalingMask compute_scaling_mask(const std::vector<double>& act_absmax,
@@ -540,17 +548,63 @@ std::pair<Matrix, Matrix> apply_balance(const Matrix& x, const Matrix& w, const 
   return {std::move(xb), std::move(wb)};
 }
 
+namespace {
+
+// fake_quantize(v, per-row group, bits, Dynamic, symmetric) in place on the
+// device: exact per-row params and codes (quant.cpp:90-177), then
+// dequantize (quant.cpp:179-188) over the same buffer
+void fake_quantize_rows_dev(double* v, std::size_t rows, std::size_t cols, int bits,
+                            bool symmetric, int grouping) {
+  const int64_t ldc = pitch16(cols);
+  Dev<uint8_t> dc(rows * ldc);
+  Dev<double> ds(rows);
+  Dev<int32_t> dz(rows), st(1);
+  cuda(cudaMemset(st.p, 0, sizeof(int32_t)));
+  check(dtq_quantize_rows(v, DTQ_F64, rows, cols, cols, bits, symmetric ? 1 : 0, DTQ_MODE_EXACT,
+                          nullptr, nullptr, dc.p, ldc, ds.p, dz.p, st.p, nullptr));
+  int32_t bad = 0;
+  st.get(&bad);
+  if (bad) throw std::invalid_argument("quantize: non-finite input");
+  check(dtq_dequantize(dc.p, rows, cols, ldc, grouping, 0, ds.p, dz.p, v, cols, nullptr));
+}
+
+}  // namespace
+
+// choose_alpha (balance.cpp:142-165) with every matrix resident on the
+// device: the reference GEMM, the column statistics, both sides of
+// apply_scaling, the per-token / per-output-channel fake quantization and the
+// quantized GEMM of each alpha.  The mask (K pow() per alpha) and the mse
+// (the reference's sequential fp64 sum, which sets the ordering of nearly
+// equal errors) stay on the host, so the chosen alpha is the reference's.
 double choose_alpha(const Matrix& calib_x, const Matrix& w, int act_bits, int weight_bits) {
-  const Matrix ref = matmul_nt(calib_x, w);
-  const std::vector<double> am = col_absmax(calib_x), wm = col_absmax(w);
+  if (calib_x.cols() != w.cols()) throw std::invalid_argument("matmul_nt: inner dimensions differ");
+  const std::size_t M = calib_x.rows(), K = calib_x.cols(), N = w.rows();
+  if (M == 0 || K == 0 || N == 0) throw std::invalid_argument("choose_alpha: empty input");
+  if (!bits_supported(act_bits) || !bits_supported(weight_bits))
+    throw std::invalid_argument("quantize: bits must be one of {2,4,6,8}");
+  Dev<double> dx(calib_x.data().data(), M * K), dw(w.data().data(), N * K);
+  Dev<double> dy(M * N), dxs(M * K), dws(N * K), dam(K), dwm(K), dsm(K);
+  check(dtq_matmul_nt_f64(dx.p, M, K, dw.p, N, nullptr, dy.p, nullptr));
+  Matrix ref(M, N);
+  dy.get(ref.data().data());
+  std::vector<double> am(K), wm(K);
+  check(dtq_col_absmax_f64(dx.p, M, K, K, dam.p, nullptr));
+  check(dtq_col_absmax_f64(dw.p, N, K, K, dwm.p, nullptr));
+  dam.get(am.data());
+  dwm.get(wm.data());
   double best_alpha = 0.5, best = std::numeric_limits<double>::infinity();
+  Matrix yq(M, N);
   for (int step = 1; step <= 9; ++step) {
     const double alpha = 0.1 * step;
-    const auto [xs, ws] = apply_scaling(calib_x, w, compute_scaling_mask(am, wm, alpha));
-    const Matrix xq = fake_quantize(xs, GroupingScheme::per_token(), act_bits, QuantMode::Dynamic);
-    const Matrix wq = fake_quantize(ws, GroupingScheme::per_output_channel(), weight_bits,
-                                    QuantMode::Dynamic, nullptr, true);
-    const double err = mse(matmul_nt(xq, wq), ref);
+    const ScalingMask mask = compute_scaling_mask(am, wm, alpha);
+    cuda(cudaMemcpy(dsm.p, mask.s.data(), K * sizeof(double), cudaMemcpyHostToDevice));
+    check(dtq_balance_apply(dx.p, M, K, K, dsm.p, 0, nullptr, 0, dxs.p, K, nullptr));  // X / s
+    check(dtq_balance_apply(dw.p, N, K, K, dsm.p, 1, nullptr, 0, dws.p, K, nullptr));  // W * s
+    fake_quantize_rows_dev(dxs.p, M, K, act_bits, false, 1);      // per_token, asymmetric
+    fake_quantize_rows_dev(dws.p, N, K, weight_bits, true, 3);    // per_output_channel, symmetric
+    check(dtq_matmul_nt_f64(dxs.p, M, K, dws.p, N, nullptr, dy.p, nullptr));
+    dy.get(yq.data().data());
+    const double err = mse(yq, ref);
     if (err < best) {
       best = err;
       best_alpha = alpha;

@@ -653,14 +653,25 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
     // every thread's code / param stores of the previous tile precede this
     // barrier: publish those rows to the GEMM waiting on their block
     if (a.ready != nullptr && t == 0 && it > 0) fq_publish_rows(a, tile - gridDim.x, R);
-    if (!ok) continue;
+    // the row's min / max from the warps' partials: the 32 / R lanes of this
+    // warp that share the row (lane & (R - 1) == r) each read every
+    // (32 / R)-th partial, then a shuffle fold -- ceil(nwarp * R / 32) reads
+    // per lane instead of nwarp (every lane, before the row-validity exit)
     float mn = __int_as_float(0x7f800000), mx = -mn;
-    const int nwarp = (nb * R + kFqItems - 1) / kFqItems;  // one partial per warp
-    for (int j = 0; j < nwarp; ++j) {
-      const float2 m = red_mm[((it & 1) * nb + j) * R + r];
-      mn = fminf(mn, m.x);
-      mx = fmaxf(mx, m.y);
+    {
+      const int nwarp = (nb * R + kFqItems - 1) / kFqItems;  // one partial per warp
+      for (int j = lane / R; j < nwarp; j += 32 / R) {
+        const float2 m = red_mm[((it & 1) * nb + j) * R + r];
+        mn = fminf(mn, m.x);
+        mx = fmaxf(mx, m.y);
+      }
+#pragma unroll
+      for (int o = R; o < 32; o <<= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
     }
+    if (!ok) continue;
     if (FQ_DBG(a) == 6) {  // diagnostics: codes with fixed parameters (no parameter math)
       fq_tile_codes<kFqQ, true, kExactV>(P, 0.01f + 1e-30f * mx, 128.f + 12582912.0f, qmax_i,
                                          1.0, 100.0, 128.0, qmax,
@@ -695,8 +706,9 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
     // s = num / den in fp64 (quant.cpp:90-124); only the writer lane forms
     // it (and the rare exact re-evaluation); kExactV needs fl32(1/s) = one
     // fp64 divide den / num per thread
-    double num, den;
-    {
+    const bool writer = b == 0 && p == 0;
+    double num = 1.0, den = 1.0;  // the fp64 s = num / den: writer and exact-code lanes only
+    if (writer || kExactV) {
       const double dmn = static_cast<double>(mn), dmx = static_cast<double>(mx);
       if (a.symmetric) {
         const double amax = fmax(fabs(dmn), fabs(dmx));
@@ -710,7 +722,6 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
         den = qmax;
       }
     }
-    const bool writer = b == 0 && p == 0;
     double s = 0.0;
     if (writer) {
       s = num / den;

@@ -53,10 +53,11 @@ __global__ void dequantize_kernel(const uint8_t* __restrict__ codes, int64_t row
 
 // One CTA per (row, hblock-wide block): scale, signs, in-smem FWHT with the
 // reference butterfly order (balance.cpp:22-33), normalise.
-__global__ void balance_kernel(const double* __restrict__ x, int64_t cols, int64_t ldx,
+// raw_fwht: the butterflies alone (fwht, balance.cpp:22-33), no signs / norm.
+__global__ void balance_kernel(const double* x, int64_t cols, int64_t ldx,
                                const double* __restrict__ smooth, int smooth_mul,
-                               const int8_t* __restrict__ signs, int64_t hb,
-                               double* __restrict__ out, int64_t ldo) {
+                               const int8_t* __restrict__ signs, int64_t hb, double* out,
+                               int64_t ldo, int raw_fwht = 0) {
   extern __shared__ double buf[];
   const int64_t r = blockIdx.y;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * hb;
@@ -67,7 +68,7 @@ __global__ void balance_kernel(const double* __restrict__ x, int64_t cols, int64
     buf[c] = v;
   }
   __syncthreads();
-  if (signs) {
+  if (signs || raw_fwht) {
     for (int64_t h = 1; h < hb; h <<= 1) {
       for (int64_t p = threadIdx.x; p < hb / 2; p += blockDim.x) {
         const int64_t j = (p / h) * (2 * h) + (p % h);
@@ -168,6 +169,44 @@ __global__ void wide_params_kernel(const double2* __restrict__ part, int64_t row
   zero[r] = static_cast<int32_t>(z);
 }
 
+// col_absmax / row_absmax (matrix.hpp:95-109): max |x| per column / row in
+// fp64 -- max is exact, so any reduction order gives the reference's values
+// (fmax drops NaN like the reference's std::max(acc, |x|) with acc first).
+__global__ void col_absmax_kernel(const double* __restrict__ x, int64_t rows, int64_t cols,
+                                  int64_t ldx, int64_t rows_per, double* __restrict__ part) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= cols) return;
+  const int64_t r0 = blockIdx.y * rows_per;
+  const int64_t r1 = r0 + rows_per < rows ? r0 + rows_per : rows;
+  double m = 0.0;
+  for (int64_t r = r0; r < r1; ++r) m = fmax(m, fabs(x[r * ldx + c]));  // coalesced over c
+  part[blockIdx.y * cols + c] = m;
+}
+
+__global__ void max_fold_kernel(const double* __restrict__ part, int64_t n, int nparts,
+                                double* __restrict__ out) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= n) return;
+  double m = 0.0;
+  for (int i = 0; i < nparts; ++i) m = fmax(m, part[i * n + c]);
+  out[c] = m;
+}
+
+__global__ void row_absmax_kernel(const double* __restrict__ x, int64_t cols, int64_t ldx,
+                                  double* __restrict__ out) {
+  const int64_t r = blockIdx.x;
+  double m = 0.0;
+  for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) m = fmax(m, fabs(x[r * ldx + c]));
+  for (int o = 16; o >= 1; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    out[r] = m;
+  }
+}
+
 int grid_for(int64_t n) {
   const int64_t g = (n + 255) / 256;
   return static_cast<int>(g < 148 * 32 ? (g > 0 ? g : 1) : 148 * 32);
@@ -222,6 +261,50 @@ int dtq_balance_apply(const double* x, int64_t rows, int64_t cols, int64_t ldx,
   balance_kernel<<<grid, 256, smem, static_cast<cudaStream_t>(stream)>>>(
       x, cols, ldx, smooth, smooth_mul, signs, hb, out, ldo);
   return last_cuda("balance_apply");
+}
+
+int dtq_col_absmax_f64(const double* x, int64_t rows, int64_t cols, int64_t ldx, double* out,
+                       void* stream) {
+  if (rows <= 0 || cols <= 0 || ldx < cols || !x || !out) return DTQ_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // row slabs of 64 rows, each column's slab maxima folded in a second pass
+  const int64_t rows_per = 64;
+  const int64_t nparts = (rows + rows_per - 1) / rows_per;
+  if (nparts > 65535) return DTQ_ERR_INVALID_ARGUMENT;
+  double* part = nullptr;
+  if (cudaMallocAsync(&part, nparts * cols * sizeof(double), st) != cudaSuccess)
+    return DTQ_ERR_CUDA;
+  dim3 grid(static_cast<unsigned>((cols + 127) / 128), static_cast<unsigned>(nparts));
+  col_absmax_kernel<<<grid, 128, 0, st>>>(x, rows, cols, ldx, rows_per, part);
+  max_fold_kernel<<<static_cast<unsigned>((cols + 127) / 128), 128, 0, st>>>(
+      part, cols, static_cast<int>(nparts), out);
+  cudaFreeAsync(part, st);
+  return last_cuda("col_absmax");
+}
+
+int dtq_row_absmax_f64(const double* x, int64_t rows, int64_t cols, int64_t ldx, double* out,
+                       void* stream) {
+  if (rows <= 0 || cols <= 0 || ldx < cols || !x || !out) return DTQ_ERR_INVALID_ARGUMENT;
+  if (rows > 0x7fffffff) return DTQ_ERR_INVALID_ARGUMENT;
+  row_absmax_kernel<<<static_cast<unsigned>(rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, cols, ldx, out);
+  return last_cuda("row_absmax");
+}
+
+int dtq_fwht_f64(double* x, int64_t rows, int64_t n, int64_t ldx, void* stream) {
+  // fwht (balance.cpp:22-33) on each row, in place: the reference butterfly
+  // order (a + b low, a - b high; h = 1, 2, 4, ...), unnormalised, no signs
+  if (rows <= 0 || n <= 0 || (n & (n - 1)) != 0 || n > 16384 || ldx < n || !x)
+    return DTQ_ERR_INVALID_ARGUMENT;
+  if (n == 1) return DTQ_OK;
+  dim3 grid(1, static_cast<unsigned>(rows));
+  const size_t smem = n * sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(balance_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+  balance_kernel<<<grid, 256, smem, static_cast<cudaStream_t>(stream)>>>(
+      x, n, ldx, nullptr, 0, nullptr, n, x, ldx, /*raw_fwht=*/1);
+  return last_cuda("fwht");
 }
 
 int dtq_matmul_nt_f64(const double* x, int64_t M, int64_t K, const double* w, int64_t N,

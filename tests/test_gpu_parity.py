@@ -558,3 +558,18 @@ def test_row_flag_path_subprocess():
                        capture_output=True, text=True, env=env, timeout=600, cwd=root)
     print(r.stdout[-2000:])
     assert r.returncode == 0 and " passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_race_stress_every_tile_config():
+    # race detection by repetition (compute-sanitizer is closed on this pool):
+    # tools/race_stress.py, every GEMM tile config incl. W4 CTA pairs, each
+    # forward repeated and interleaved with other shapes -- bit-identical
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "race_stress.py"), "30"],
+                       capture_output=True, text=True, timeout=900, cwd=root)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr[-2000:]
+    assert r.stdout.count('"mismatches": 0') == 5

@@ -91,10 +91,11 @@ def lib():
     L.dtq_checkpoint_num_layers.argtypes = [p, p]
     L.dtq_checkpoint_layer_info.argtypes = [p, i64, p, p, p, p, p, p, p]
     L.dtq_checkpoint_load_layer.argtypes = [p, i64, i32, i32, p, p]
-    L.dtq_planned_create.argtypes = [p, i32, i64, i64, i64, p, i32, p, p, p, p]
-    L.dtq_planned_destroy.argtypes = [p]
-    L.dtq_planned_select.argtypes = [p, i64, i64, p]
-    L.dtq_planned_bits.argtypes = [p, i32, p]
+    if hasattr(L, "dtq_planned_create"):  # (an older library via DTQ_B200_LIB lacks them)
+        L.dtq_planned_create.argtypes = [p, i32, i64, i64, i64, p, i32, p, p, p, p]
+        L.dtq_planned_destroy.argtypes = [p]
+        L.dtq_planned_select.argtypes = [p, i64, i64, p]
+        L.dtq_planned_bits.argtypes = [p, i32, p]
     _lib = L
     return L
 

@@ -35,9 +35,11 @@ inline cudaError_t fq_tile_occupancy(const void* kern, int block, size_t smem, i
     // the whole unified L1 / shared array as shared memory: an SM running
     // this kernel can then also host the co-resident GEMM CTA (the carveout
     // is fixed while any CTA is resident on the SM)
+#ifndef DTQ_NO_CARVEOUT
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
+#endif
     mx = smem;
   }
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, block, smem);

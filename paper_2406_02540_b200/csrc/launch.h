@@ -58,9 +58,11 @@ cudaError_t dtq_launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB,
   if (configured_dev != dev) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::alloc);
     if (e != cudaSuccess) return e;
+#ifndef DTQ_NO_CARVEOUT
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
+#endif
     configured_dev = dev;
   }
   const int tiles = g.tiles_m * g.tiles_n;

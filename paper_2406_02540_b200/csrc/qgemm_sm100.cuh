@@ -193,7 +193,11 @@ __device__ __forceinline__ uint2 w4_word_to_s8x8_x16(uint32_t w) {
 // capped at 112 registers per thread so both CTAs' registers fit the SM (the
 // others at 200, what 320 threads of one CTA per SM allow anyway).
 template <int BN, int kStages, bool kW4, int kOut, bool k2Cta, bool kCoRes = false>
+#ifdef DTQ_PLAIN_LB
+__global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
+#else
 __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1) __maxnreg__(kCoRes ? DTQ_CORES_MAXNREG : 200)
+#endif
     qgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmY, const GemmArgs g) {
   using namespace dtq_ptx;

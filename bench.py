@@ -618,10 +618,25 @@ def run_c2(args, dev, world, stream, local):
 
     k_steps()
     torch.cuda.synchronize()
-    # host cost of the API call, eager (reported; not in the timed region)
+    # host cost of the API call, eager (reported; not in the timed region):
+    # through the Python wrapper, and through the C ABI alone (ctypes with
+    # prebuilt arguments: the cost a C/C++ caller of dtq_qlinear_forward sees,
+    # plus ~1-2 us of ctypes)
     h_start = time.perf_counter()
     k_steps()
     r["h_issue"] = (time.perf_counter() - h_start) / args.steps
+    torch.cuda.synchronize()
+    import ctypes as C
+    lib = dtq.lib()
+    cargs = [(C.c_void_p(sxring[j].data_ptr()), dtq.F16, M, K, lring[j]._h, dtq.MODE_FAST, None,
+              C.c_void_p(syring[j].data_ptr()), dtq.F16, N, C.c_void_p(ws.data_ptr()),
+              C.c_size_t(ws.numel()), None, C.c_void_p(stream.cuda_stream))
+             for j in range(nstep_ring)]
+    fwd = lib.dtq_qlinear_forward
+    h_start = time.perf_counter()
+    for i in range(args.steps):
+        fwd(*cargs[i % nstep_ring])
+    r["h_issue_cabi"] = (time.perf_counter() - h_start) / args.steps
     torch.cuda.synchronize()
     # the K timed steps are captured once as a CUDA graph (the quantizer ->
     # GEMM pairs keep their programmatic-dependent-launch edges)
@@ -800,9 +815,10 @@ def run_ours(args, world, rank, local):
                  "fused_forward_call": r["t_fwd"] * 1e3,
                  "fused_forward_call_l2_flushed": r["t_flushed"] * 1e3,
                  "host_issue_per_step": r["h_issue"] * 1e3,
+                 "host_issue_per_step_c_abi": r["h_issue_cabi"] * 1e3,
                  "note": "fused_forward_call: one layer.forward per step (both kernels), K steps "
                          "back to back over a >L2 ring, captured as one CUDA graph, one event "
-                         "pair; host_issue_per_step: the eager API call; _l2_flushed: 512 MB "
+                         "pair; host_issue_per_step: the eager Python API call (_c_abi: the C ABI call alone, ctypes with prebuilt arguments); _l2_flushed: 512 MB "
                          "write before each step, one event pair per step; per-kernel: median "
                          "of CUDA-graph batches of back-to-back launches over a >L2 input ring"}
     c2_extra = {

@@ -116,20 +116,38 @@ def _torch():
     return torch
 
 
+_DTYPES = None
+
+
 def _dtype_code(t) -> int:
-    torch = _torch()
-    return {torch.float16: F16, torch.bfloat16: BF16, torch.float32: F32, torch.float64: F64,
-            torch.int32: S32}[t]
+    global _DTYPES
+    if _DTYPES is None:
+        torch = _torch()
+        _DTYPES = {torch.float16: F16, torch.bfloat16: BF16, torch.float32: F32,
+                   torch.float64: F64, torch.int32: S32}
+    return _DTYPES[t]
 
 
 def _ptr(t) -> Optional[int]:
     return None if t is None else t.data_ptr()
 
 
+_RAW_STREAM = None
+
+
 def _stream(stream=None) -> int:
+    """The cudaStream_t to launch on: `stream`, else torch's current stream
+    of the current device (read without building a Stream object: this runs
+    on every call)."""
+    global _RAW_STREAM
+    if stream is not None:
+        return stream.cuda_stream
     torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if _RAW_STREAM is None:
+        _RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", False)
+    if _RAW_STREAM:
+        return _RAW_STREAM(torch.cuda.current_device())
+    return torch.cuda.current_stream().cuda_stream
 
 
 @dataclass

@@ -8,6 +8,7 @@
 //
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 \
 //          -I../paper_2406_02540_b200/csrc l2_smem_probe.cu -o _bin/l2_smem_probe
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -147,6 +148,68 @@ __global__ void __launch_bounds__(128, 1) pipeline(int stages, int kblocks,
   }
 }
 
+// The same pipeline with the GEMM's own loads: TMA 2D boxes (128 rows x
+// 128 B, SWIZZLE_128B) from a row-major [rows, 1152] u8 tensor (A: one box,
+// B: two boxes of 128 rows) -- 128-byte row segments at a 1152-byte pitch.
+__global__ void __launch_bounds__(128, 1) pipeline_tma(int stages, int kblocks, int rows,
+                                                       const __grid_constant__ CUtensorMap tm) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  constexpr int kStage = 49152;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * kStage);
+  uint64_t* empty = full + stages;
+  uint64_t* done = empty + stages;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(done + 1);
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tm);
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 1);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc<512>(slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  if (threadIdx.x == 32) {  // producer
+    int m = (blockIdx.x * 384) % (rows - 384);
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % stages;
+      mbar_wait(empty + s, ((kb / stages) & 1) ^ 1);
+      mbar_arrive_expect_tx(full + s, kStage);
+      const int k = (kb % 9) * 128;
+      tma_load_2d(smem + s * kStage, &tm, full + s, k, m);
+      tma_load_2d(smem + s * kStage + 16384, &tm, full + s, k, m + 128);
+      tma_load_2d(smem + s * kStage + 32768, &tm, full + s, k, m + 256);
+      if (kb % 9 == 8) m = (m + 148 * 384) % (rows - 384);
+    }
+  } else if (threadIdx.x == 0) {  // MMA issuer
+    constexpr uint32_t idesc = idesc_i8_u8s8(128, 256);
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % stages;
+      mbar_wait(full + s, (kb / stages) & 1);
+      tc_fence_after();
+      const uint64_t ad = umma_desc_sw128(smem_u32(smem + s * kStage));
+      const uint64_t bd = umma_desc_sw128(smem_u32(smem + s * kStage + 16384));
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        mma_i8(tmem + ((kb / 9) & 1) * 256, ad + 2 * k, bd + 2 * k, idesc, (kb % 9 | k) != 0 ? 1u : 0u);
+      mma_commit(empty + s);
+    }
+    mma_commit(done);
+    mbar_wait(done, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 int main() {
   const int sms = 148;
   const int64_t span = 10 << 20;  // 10 MB: the C2 GEMM's A + B footprint, L2-resident
@@ -177,6 +240,40 @@ int main() {
     printf("{\"mode\": \"%s\", \"ms\": %.3f, \"mma_tops\": %.0f, \"copy_tbs\": %.2f, \"err\": \"%s\"}\n",
            names[mode], ms, (mode & 1) ? ops / (ms * 1e-3) / 1e12 : 0.0,
            (mode & 2) ? bytes / (ms * 1e-3) / 1e12 : 0.0, cudaGetErrorString(cudaGetLastError()));
+  }
+  {
+    // TMA 2D boxes over a [rows, 1152] u8 tensor (L2-resident 9.4 MB)
+    const int rows = 8192;
+    uint8_t* t;
+    cudaMalloc(&t, (size_t)rows * 1152);
+    cudaMemset(t, 3, (size_t)rows * 1152);
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {1152, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {1152};
+    cuuint32_t box[2] = {128, 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, t, dims, strides, box,
+                                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) printf("encode failed %d\n", (int)r);
+    for (int stages = 3; stages <= 4; ++stages) {
+      const int sm2 = stages * 49152 + 2 * stages * 8 + 64 + 1024;
+      cudaFuncSetAttribute(pipeline_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+      pipeline_tma<<<sms, 128, sm2>>>(stages, 450, rows, tm);
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a);
+      pipeline_tma<<<sms, 128, sm2>>>(stages, 4005, rows, tm);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      const double ops = 2.0 * 128 * 256 * 128 * 4005.0 * sms;
+      printf("{\"mode\": \"gemm pipeline, TMA 2D boxes, %d x 48 KB stages\", \"ms\": %.3f, \"mma_tops\": %.0f, \"err\": \"%s\"}\n",
+             stages, ms, ops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+    }
   }
   for (int stages = 2; stages <= 4; ++stages) {
     const int sm2 = stages * 49152 + 2 * stages * 8 + 64 + 1024;

@@ -21,6 +21,10 @@ KEYS = [
     "launch__shared_mem_per_block_dynamic",
     "sm__pipe_tensor_op_imma_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tensor_subpipe_imma.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
     "lts__t_sectors_srcunit_tex_op_write.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
 ]
 

@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/dtq_capi.h"
 #include "launch.h"
 
@@ -28,6 +30,14 @@ int dtq_quantize_rows_wide_f64(const double* x, int64_t rows, int64_t cols, int6
                                int32_t* zero, int32_t* status, cudaStream_t st);
 
 namespace {
+
+// NVTX range over a C-ABI call (header-only NVTX3: a few ns when no tool is
+// attached; Nsight Systems / ncu --nvtx show the host calls around the
+// kernels they launch)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 thread_local std::string g_last_error;
 
@@ -1074,6 +1084,7 @@ int dtq_quantize_rows(const void* x, int x_dtype, int64_t rows, int64_t cols, in
                       int bits, int symmetric, int mode, const dtq_balance* balance,
                       const dtq_prologue* prologue, uint8_t* codes, int64_t ldc, double* scale,
                       int32_t* zero, int32_t* status, void* stream) {
+  NvtxRange nvtx_range("dtq_quantize_rows");
   const double* smooth = balance ? balance->smooth : nullptr;
   const int8_t* signs = balance ? balance->signs : nullptr;
   const int hblock = balance ? balance->hblock : 0;
@@ -1101,6 +1112,7 @@ int dtq_quantize_rows(const void* x, int x_dtype, int64_t rows, int64_t cols, in
 int dtq_qlinear_create(const void* w, int w_dtype, int64_t N, int64_t K, int64_t ldw,
                        int weight_bits, int act_bits, const double* bias,
                        const dtq_balance* balance, void* stream, dtq_qlinear_t* out) {
+  NvtxRange nvtx_range("dtq_qlinear_create");
   if (!out) return fail(DTQ_ERR_INVALID_ARGUMENT, "create: null out");
   *out = nullptr;
   if (!bits_supported(weight_bits))
@@ -1160,6 +1172,7 @@ int dtq_qlinear_create_from_codes(const uint8_t* codes, int packed, int64_t ld, 
                                   const double* scale, int64_t N, int64_t K, int act_bits,
                                   const double* bias, const dtq_balance* balance, void* stream,
                                   dtq_qlinear_t* out) {
+  NvtxRange nvtx_range("dtq_qlinear_create_from_codes");
   if (!out) return fail(DTQ_ERR_INVALID_ARGUMENT, "create: null out");
   *out = nullptr;
   if (!bits_supported(weight_bits))
@@ -1239,6 +1252,7 @@ int dtq_qlinear_export(dtq_qlinear_t h, uint8_t* codes, double* scale, int32_t* 
 
 int dtq_qgemm(const uint8_t* codes, int64_t ldc, const double* s_x, const int32_t* z_x, int64_t M,
               dtq_qlinear_t h, void* y, int y_dtype, int64_t ldy, void* stream) {
+  NvtxRange nvtx_range("dtq_qgemm");
   return qgemm_impl(codes, ldc, s_x, z_x, M, h, y, y_dtype, ldy, as_stream(stream));
 }
 
@@ -1253,6 +1267,7 @@ int dtq_qlinear_forward(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_
                         int mode, const dtq_prologue* prologue, void* y, int y_dtype,
                         int64_t ldy, void* workspace, size_t workspace_bytes, int32_t* status,
                         void* stream) {
+  NvtxRange nvtx_range("dtq_qlinear_forward");
   return forward_impl(x, x_dtype, M, ldx, h, mode, prologue, y, y_dtype, ldy, workspace,
                       workspace_bytes, status, as_stream(stream));
 }
@@ -1260,6 +1275,7 @@ int dtq_qlinear_forward(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_
 int dtq_qlinear_quantize(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear_t h,
                          int mode, const dtq_prologue* prologue, uint8_t* codes, int64_t ldc,
                          double* scale, int32_t* zero, int32_t* status, void* stream) {
+  NvtxRange nvtx_range("dtq_qlinear_quantize");
   if (!h) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: null handle");
   if (ldx < h->K) return fail(DTQ_ERR_INVALID_ARGUMENT, "qlinear_forward: X cols != C_in");
   return quantize_rows_impl(x, x_dtype, M, h->K, ldx, h->abits, 0, mode, 0, h->smooth,
@@ -1269,6 +1285,7 @@ int dtq_qlinear_quantize(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq
 
 int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_t h, int mode,
                              void* y, int y_dtype, void* stream) {
+  NvtxRange nvtx_range("dtq_qlinear_forward_host");
   if (!h || !x || !y || M <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "forward_host: bad args");
   const size_t xe = dtype_size(x_dtype), ye = dtype_size(y_dtype);
   const size_t xb = xe * static_cast<size_t>(M) * h->K;
@@ -1427,6 +1444,7 @@ int dtq_checkpoint_layer_info(dtq_checkpoint_t ck, int64_t i, const char** name,
 
 int dtq_checkpoint_load_layer(dtq_checkpoint_t ck, int64_t i, int act_bits, int hblock,
                               void* stream, dtq_qlinear_t* out) {
+  NvtxRange nvtx_range("dtq_checkpoint_load_layer");
   if (!out) return fail(DTQ_ERR_INVALID_ARGUMENT, "checkpoint_load_layer: null out");
   *out = nullptr;
   if (!ck || i < 0 || i >= static_cast<int64_t>(ck->layers.size()))
@@ -1498,6 +1516,7 @@ int dtq_checkpoint_load_layer(dtq_checkpoint_t ck, int64_t i, int act_bits, int 
 int dtq_planned_create(const void* w, int w_dtype, int64_t N, int64_t K, int64_t ldw,
                        const int32_t* bits, int act_bits, const double* bias,
                        const dtq_balance* balance, void* stream, dtq_planned_t* out) {
+  NvtxRange nvtx_range("dtq_planned_create");
   if (!out || !bits) return fail(DTQ_ERR_INVALID_ARGUMENT, "planned_create: null argument");
   *out = nullptr;
   for (int r = 0; r < kPlanRanges; ++r)

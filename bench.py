@@ -179,15 +179,27 @@ class ClockSampler:
                 "source": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
+# DTQ_BENCH_SINGLE_GPU_RANKS=1 (path check only, never a bench number):
+# every rank on cuda:0 and gloo for the collectives, so the N > 1 code path
+# runs end to end on a one-GPU box (the kernels of different ranks never
+# wait on each other)
+_SINGLE_GPU_RANKS = os.environ.get("DTQ_BENCH_SINGLE_GPU_RANKS") == "1"
+
+
 def dist_setup():
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if _SINGLE_GPU_RANKS:
+        local = 0
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if _SINGLE_GPU_RANKS:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
@@ -198,7 +210,7 @@ def max_over_ranks(v: float, world: int) -> float:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device="cpu" if _SINGLE_GPU_RANKS else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -552,7 +564,9 @@ def run_c5(args, dev, world, rank, stream, local, verify=True):
                   "api": "QuantLinear.forward over the stack, pinned host in/out"}
     del gr
     if verify and world > 1:
-        y_all = gather_rows(y_local, C5_IMG)   # NCCL all_gather over NVLink
+        y_all = gather_rows(y_local.cpu() if _SINGLE_GPU_RANKS else y_local,
+                            C5_IMG)   # NCCL all_gather over NVLink
+        y_all = y_all.to(dev)
         ok = None
         if rank == 0:
             del bufs

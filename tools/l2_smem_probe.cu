@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "ptx.cuh"
 
@@ -210,6 +211,72 @@ __global__ void __launch_bounds__(128, 1) pipeline_tma(int stages, int kblocks, 
   }
 }
 
+// The CTA-pair pipeline of the product GEMM (cta_group::2, 256 x 256 tiles):
+// per k-block each CTA TMA-loads its 128 A rows and its 128 of the 256 B rows
+// (16 + 16 KB) completing on the LEADER's full barrier; the leader issues
+// 4 x tcgen05.mma.cta_group::2 and multicasts the commit to both CTAs' empty
+// barriers, on which each CTA's producer waits before refilling.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    pipeline_pair(int stages, int kblocks, int rows, const __grid_constant__ CUtensorMap tm) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  constexpr int kStage = 32768;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * kStage);
+  uint64_t* empty = full + stages;
+  uint64_t* done = empty + stages;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(done + 1);
+  const uint32_t rank = cluster_ctarank();
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tm);
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 1);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc_cta2<512>(slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  if (threadIdx.x == 32) {  // producer (both CTAs)
+    int m = ((blockIdx.x >> 1) * 512) % (rows - 512);
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % stages;
+      mbar_wait(empty + s, ((kb / stages) & 1) ^ 1);
+      const uint32_t lead_full = mapa_shared(smem_u32(full + s), 0);
+      if (rank == 0) mbar_arrive_expect_tx(full + s, 2 * kStage);
+      const int k = (kb % 9) * 128;
+      tma_load_2d_2sm(smem + s * kStage, &tm, lead_full, k, m + rank * 128);
+      tma_load_2d_2sm(smem + s * kStage + 16384, &tm, lead_full, k, m + 256 + rank * 128);
+      if (kb % 9 == 8) m = (m + 74 * 512) % (rows - 512);
+    }
+  } else if (threadIdx.x == 0 && rank == 0) {  // leader MMA issuer
+    constexpr uint32_t idesc = idesc_i8_u8s8(256, 256);
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % stages;
+      mbar_wait(full + s, (kb / stages) & 1);
+      tc_fence_after();
+      const uint64_t ad = umma_desc_sw128(smem_u32(smem + s * kStage));
+      const uint64_t bd = umma_desc_sw128(smem_u32(smem + s * kStage + 16384));
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        mma_i8_cta2(tmem + ((kb / 9) & 1) * 256, ad + 2 * k, bd + 2 * k, idesc,
+                    (kb % 9 | k) != 0 ? 1u : 0u);
+      mma_commit_cta2_mc(empty + s, 0x3);
+    }
+    mma_commit_cta2_mc(done, 0x3);
+  }
+  if (threadIdx.x == 0) mbar_wait(done, 0);
+  tc_fence_before();
+  cluster_sync();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    tmem_dealloc_cta2<512>(tmem);
+  }
+}
+
 int main() {
   const int sms = 148;
   const int64_t span = 10 << 20;  // 10 MB: the C2 GEMM's A + B footprint, L2-resident
@@ -247,6 +314,16 @@ int main() {
     uint8_t* t;
     cudaMalloc(&t, (size_t)rows * 1152);
     cudaMemset(t, 3, (size_t)rows * 1152);
+    if (getenv("PROBE_RANDOM")) {  // random bytes: the MMA's data-dependent power
+      uint8_t* h = (uint8_t*)malloc((size_t)rows * 1152);
+      uint32_t x = 12345;
+      for (size_t i = 0; i < (size_t)rows * 1152; ++i) {
+        x = x * 1664525u + 1013904223u;
+        h[i] = (uint8_t)(x >> 24);
+      }
+      cudaMemcpy(t, h, (size_t)rows * 1152, cudaMemcpyHostToDevice);
+      free(h);
+    }
     CUtensorMap tm;
     cuuint64_t dims[2] = {1152, (cuuint64_t)rows};
     cuuint64_t strides[1] = {1152};
@@ -257,6 +334,23 @@ int main() {
                                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) printf("encode failed %d\n", (int)r);
+    for (int stages = 4; stages <= 6; ++stages) {
+      const int sm3 = stages * 32768 + 2 * stages * 8 + 64 + 1024;
+      cudaFuncSetAttribute(pipeline_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3);
+      pipeline_pair<<<sms, 128, sm3>>>(stages, 450, rows, tm);
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a);
+      pipeline_pair<<<sms, 128, sm3>>>(stages, 4005, rows, tm);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      const double ops = 2.0 * 256 * 256 * 128 * 4005.0 * (sms / 2);
+      printf("{\"mode\": \"CTA-pair pipeline, TMA 2D boxes, %d x 32 KB stages per CTA\", \"ms\": %.3f, \"mma_tops\": %.0f, \"err\": \"%s\"}\n",
+             stages, ms, ops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+    }
     for (int stages = 3; stages <= 4; ++stages) {
       const int sm2 = stages * 49152 + 2 * stages * 8 + 64 + 1024;
       cudaFuncSetAttribute(pipeline_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);

@@ -805,6 +805,18 @@ def rooflines(r):
           "at_M16384": {"ms": r["t_fq16"] * 1e3, "achieved": fq_bytes16 / r["t_fq16"] / 1e9,
                         "frac": fq_bytes16 / r["t_fq16"] / 1e9 / hbm, "bytes": fq_bytes16,
                         "note": "same kernel at the stack's 16384 rows"}}
+    # the whole step against its two floors: all its HBM bytes at the measured
+    # copy bandwidth (the GEMM's output written back included, which a single
+    # launch hides in L2) and its INT8 ops at the measured tensor ceiling
+    step_bytes = fq_bytes + gemm_bytes - M * K      # the codes stay in L2 between the two
+    floors = {"hbm_us": step_bytes / (hbm * 1e9) * 1e6, "tensor_us": ops / (peak * 1e12) * 1e6}
+    step = {"bytes": step_bytes, "ops": ops, **floors,
+            "step_us": r["t_fwd"] * 1e6, "step_l2_flushed_us": r["t_flushed"] * 1e6,
+            "frac_of_max_floor": max(floors.values()) / (r["t_fwd"] * 1e6),
+            "frac_of_sum_of_floors": sum(floors.values()) / (r["t_fwd"] * 1e6),
+            "note": "max floor = perfect overlap of the memory and tensor work; sum = the "
+                    "two run back to back (quantizer, then GEMM)"}
+    roof["step"] = step
     return roof, fq
 
 

@@ -425,7 +425,13 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
         ld16<Tin>(src + 16 * kFqQ * m * es, lo);
         ld16<Tin>(src + (16 * kFqQ * m + 64) * es, hi);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) P[16 * m + i] = make_float2(lo[i], hi[i]);
+        for (int i = 0; i < 16; ++i) {
+          P[16 * m + i] = make_float2(lo[i], hi[i]);
+          // GELU as the values arrive, 16 pairs at a time: fewer values live
+          // beside its temporaries than in one pass over all of P (the
+          // 576-thread wide variant is capped at 96 registers)
+          if constexpr (kPro == kProGelu) P[16 * m + i] = gelu2(P[16 * m + i]);
+        }
       }
     }
 
@@ -446,10 +452,7 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
       continue;
     }
     // ---- 2. prologue
-    if constexpr (kPro == kProGelu) {
-#pragma unroll
-      for (int k = 0; k < kFqPairs; ++k) P[k] = gelu2(P[k]);
-    } else if constexpr (kPro == kProLnModulate) {
+    if constexpr (kPro == kProLnModulate) {
       // LayerNorm statistics in ONE exchange: per-thread mean and M2 (two
       // passes over registers), merged across the lanes of a block and then
       // across the row's blocks with Chan et al.'s pairwise update (equal

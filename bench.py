@@ -88,8 +88,9 @@ def make_inputs(seed: int = 1234, rows: int = M):
 class ClockSampler:
     """SM clocks + throttle reasons sampled DURING the timed region.
 
-    NVML (nvidia-ml-py) polled from a thread every ~1 ms -- the timed region
-    can be a few ms long -- with `nvidia-smi -lms 20` as the fallback.
+    NVML (nvidia-ml-py) polled from a thread every ~0.1 ms plus the query
+    time -- the timed region can be under a millisecond -- with
+    `nvidia-smi -lms 20` as the fallback.
     """
 
     # nvmlClocksEventReason* bits
@@ -143,7 +144,7 @@ class ClockSampler:
                 self.samples.append((sm, self.mx, {n for n, b in self.BITS.items() if r & b}))
             except Exception:
                 pass
-            time.sleep(0.0005)
+            time.sleep(0.0001)
 
     def _read(self):
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]

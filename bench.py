@@ -392,9 +392,11 @@ def run_stack(dev, reps: int = 10):
     x = (torch.randn((STACK_IMG, 1152), generator=g, device=dev) * 2).half()
     txt = torch.randn((STACK_TXT, 1152), generator=g, device=dev).half()
     res = {}
-    for key, plan in (("w8a8", uniform_plan(PIXART_LAYERS, STACK_BLOCKS, 8)),
-                      ("w4a8_mp", w4a8_mp_plan(PIXART_LAYERS, STACK_BLOCKS))):
-        st = LinearStack(PIXART_LAYERS, STACK_BLOCKS, plan, dev, seed=7)
+    for key, plan, epi in (("w8a8", uniform_plan(PIXART_LAYERS, STACK_BLOCKS, 8), True),
+                           ("w8a8_gelu_prologue", uniform_plan(PIXART_LAYERS, STACK_BLOCKS, 8),
+                            False),
+                           ("w4a8_mp", w4a8_mp_plan(PIXART_LAYERS, STACK_BLOCKS), True)):
+        st = LinearStack(PIXART_LAYERS, STACK_BLOCKS, plan, dev, seed=7, gelu_in_fc1_epilogue=epi)
         bufs = st.buffers(shape)
         # denoising step 12 of 20: range 2 (the mixed plan's W4 cells)
         gr = graph_of(lambda: st.forward(bufs, x, txt, t=12, steps=20))
@@ -415,37 +417,53 @@ def run_stack(dev, reps: int = 10):
     xb = [torch.empty_like(x) for _ in range(2)]
     h = torch.empty((STACK_IMG, 4608), dtype=torch.float16, device=dev)
 
-    def fp16(prologues: bool):
+    zb = torch.zeros(4608, dtype=torch.float16, device=dev)
+
+    def fp16(prologues: bool, gelu_epilogue: bool = False):
+        nonlocal h
         cur = x
         for b in range(STACK_BLOCKS):
             for (name, k, n, src, pro), w in zip(PIXART_LAYERS, wts[b]):
                 inp = txt if src == "txt" else (h if src == "fc1" else cur)
                 if prologues and pro == "ln_mod":
                     inp = F.layer_norm(inp, (k,), eps=1e-6) * (1 + sc) + sh
-                elif prologues and pro == "gelu":
+                elif prologues and pro == "gelu" and not gelu_epilogue:
                     inp = F.gelu(inp)
+                if gelu_epilogue and name.endswith("fc1"):
+                    # cuBLASLt's GELU epilogue (what FP16 can fuse)
+                    h = torch._addmm_activation(zb, inp, w.t(), use_gelu=True)
+                    continue
                 out = h if name.endswith("fc1") else (xb[b % 2] if name.endswith("fc2")
                                                      else outs[n])
                 torch.matmul(inp, w.t(), out=out)
             cur = xb[b % 2]
 
-    for key, pro in (("fp16_cublas", True), ("fp16_cublas_gemm_only", False)):
-        gr = graph_of(lambda: fp16(pro))
-        res[key] = float(np.median(time_graph(gr, reps)))
-        del gr
+    for key, pro, ge in (("fp16_cublas", True, False), ("fp16_cublas_gemm_only", False, False),
+                         ("fp16_cublas_gelu_epilogue", True, True)):
+        try:
+            gr = graph_of(lambda: fp16(pro, ge))
+            res[key] = float(np.median(time_graph(gr, reps)))
+            del gr
+        except Exception:  # the fused-epilogue comparator is best effort
+            res[key] = float("nan")
     ms = {k: v * 1e3 for k, v in res.items() if not k.startswith("mp_")}
     return {"workload": "PixArt-alpha 28-block linear stack, batch 4, 1024px (16384 image + 480 "
                         "text tokens), 196 linears/forward, every linear a PlannedLinear "
                         "(MixedPrecisionPlan dispatch at step 12 of 20), CUDA graphs",
             "ms": ms["w8a8"], "tops": ops / res["w8a8"] / 1e12,
+            "gelu": "in fc1's GEMM epilogue (dtq_qlinear_forward_act); fc2 quantizes as is",
+            "w8a8_gelu_in_fc2_prologue_ms": ms["w8a8_gelu_prologue"],
             "w4a8_mp_ms": ms["w4a8_mp"], "w4a8_mp_avg_bits": res["mp_avg_bits"],
             "w4a8_mp_w4_share_at_range2": res["mp_w4_share"],
             "fp16_cublas_ms": ms["fp16_cublas"],
+            "fp16_cublas_gelu_epilogue_ms": ms["fp16_cublas_gelu_epilogue"],
             "fp16_cublas_gemm_only_ms": ms["fp16_cublas_gemm_only"],
+            "speedup_vs_fp16_gelu_epilogue": res["fp16_cublas_gelu_epilogue"] / res["w8a8"],
             "speedup_vs_fp16": res["fp16_cublas"] / res["w8a8"],
             "speedup_vs_fp16_gemm_only": res["fp16_cublas_gemm_only"] / res["w8a8"],
-            "note": "fp16_cublas: eager LN / modulate / GELU + torch.matmul; gemm_only: the "
-                    "GEMMs alone, the lower bound of any fused FP16 prologue",
+            "note": "fp16_cublas: eager LN / modulate / GELU + torch.matmul; _gelu_epilogue: "
+                    "the same with fc1's GELU in cuBLASLt's epilogue; gemm_only: the GEMMs "
+                    "alone, the lower bound of any fused FP16 prologue",
             "ops": ops}
 
 

@@ -182,6 +182,17 @@ int dtq_qlinear_forward(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_
                         int64_t ldy, void* workspace, size_t workspace_bytes,
                         int32_t* status, void* stream);
 
+/* dtq_qlinear_forward with an activation applied to y in the GEMM's epilogue,
+ * on the fp32 value before the cast: DTQ_ACT_GELU gives
+ * gelu(qlinear_forward(x)) (toydit.cpp:83) in the same pass -- the fc1 ->
+ * gelu step of toydit.cpp:215-216, so the next layer's quantizer runs with no
+ * prologue.  F16 / BF16 outputs (else DTQ_ERR_UNSUPPORTED). */
+typedef enum dtq_activation { DTQ_ACT_NONE = 0, DTQ_ACT_GELU = 1 } dtq_activation;
+int dtq_qlinear_forward_act(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear_t h,
+                            int mode, const dtq_prologue* prologue, int activation, void* y,
+                            int y_dtype, int64_t ldy, void* workspace, size_t workspace_bytes,
+                            int32_t* status, void* stream);
+
 /* The quantizer stage of dtq_qlinear_forward alone: the activation side of
  * the handle's balance (X / s with the handle's fp32 reciprocals in FAST
  * mode, fp64 divide in EXACT mode, then the rotation) + optional prologue +

@@ -30,6 +30,7 @@ LIB_PATH = os.environ.get("DTQ_B200_LIB") or os.path.join(HERE, "libdtq_b200.so"
 F16, BF16, F32, F64, S32 = 0, 1, 2, 3, 4
 MODE_FAST, MODE_EXACT = 0, 1
 PROLOGUE_NONE, PROLOGUE_MODULATE, PROLOGUE_GELU, PROLOGUE_LN_MODULATE = 0, 1, 2, 3
+ACT_NONE, ACT_GELU = 0, 1
 
 DTQ_OK, DTQ_ERR_INVALID_ARGUMENT, DTQ_ERR_OVERFLOW, DTQ_ERR_CUDA, DTQ_ERR_UNSUPPORTED = range(5)
 
@@ -43,7 +44,7 @@ EXPORTED = (
     "dtq_checkpoint_open", "dtq_checkpoint_close", "dtq_checkpoint_num_layers",
     "dtq_checkpoint_layer_info", "dtq_checkpoint_load_layer",
     "dtq_planned_create", "dtq_planned_destroy", "dtq_planned_select", "dtq_planned_bits",
-    "dtq_col_absmax_f64", "dtq_row_absmax_f64", "dtq_fwht_f64",
+    "dtq_col_absmax_f64", "dtq_row_absmax_f64", "dtq_fwht_f64", "dtq_qlinear_forward_act",
 )
 
 
@@ -84,6 +85,9 @@ def lib():
     L.dtq_qlinear_workspace_bytes.restype = C.c_size_t
     L.dtq_qlinear_workspace_bytes.argtypes = [p, i64]
     L.dtq_qlinear_forward.argtypes = [p, i32, i64, i64, p, i32, p, p, i32, i64, p, C.c_size_t, p, p]
+    if hasattr(L, "dtq_qlinear_forward_act"):
+        L.dtq_qlinear_forward_act.argtypes = [p, i32, i64, i64, p, i32, p, i32, p, i32, i64, p,
+                                              C.c_size_t, p, p]
     L.dtq_qlinear_quantize.argtypes = [p, i32, i64, i64, p, i32, p, p, i64, p, p, p, p]
     L.dtq_qlinear_forward_host.argtypes = [p, i32, i64, p, i32, p, i32, p]
     L.dtq_checkpoint_open.argtypes = [C.c_char_p, p]
@@ -338,8 +342,9 @@ class QuantLinear:
 
     def forward(self, x, out_dtype=None, mode: int = MODE_FAST,
                 prologue: Optional[Prologue] = None, out=None, workspace=None, status=None,
-                stream=None):
-        """qlinear_forward(x, layer): fused quantizer + GEMM, stream-ordered."""
+                stream=None, activation: int = ACT_NONE):
+        """qlinear_forward(x, layer): fused quantizer + GEMM, stream-ordered;
+        `activation=ACT_GELU` applies GELU to y in the GEMM's epilogue."""
         torch = _torch()
         _check_rows(x, self.K, "qlinear_forward")
         M = x.shape[0]
@@ -351,6 +356,13 @@ class QuantLinear:
                                       or not workspace.is_contiguous()):
             raise ValueError("qlinear_forward: workspace must be a contiguous uint8 CUDA tensor")
         ws_ptr, ws_n = (None, 0) if workspace is None else (workspace.data_ptr(), workspace.numel())
+        if activation != ACT_NONE:
+            _check(lib().dtq_qlinear_forward_act(x.data_ptr(), _dtype_code(x.dtype), M, x.stride(0),
+                                                 self._h, mode, _ref_or_none(pr), activation,
+                                                 out.data_ptr(), _dtype_code(out.dtype),
+                                                 out.stride(0), ws_ptr, ws_n, _ptr(status),
+                                                 _stream(stream)))
+            return out
         _check(lib().dtq_qlinear_forward(x.data_ptr(), _dtype_code(x.dtype), M, x.stride(0),
                                          self._h, mode, _ref_or_none(pr), out.data_ptr(),
                                          _dtype_code(out.dtype), out.stride(0), ws_ptr, ws_n,

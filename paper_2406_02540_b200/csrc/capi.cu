@@ -772,7 +772,11 @@ unsigned long long* probe_buffer() {
 
 int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32_t* z_x,
                int64_t M, dtq_qlinear_s* h, void* y, int y_dtype, int64_t ldy, cudaStream_t st,
-               uint32_t* ready = nullptr) {
+               uint32_t* ready = nullptr, int act = DTQ_ACT_NONE) {
+  if (act != DTQ_ACT_NONE && act != DTQ_ACT_GELU)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: bad activation %d", act);
+  if (act != DTQ_ACT_NONE && !(y_dtype == DTQ_F16 || y_dtype == DTQ_BF16))
+    return fail(DTQ_ERR_UNSUPPORTED, "qgemm: the activation epilogue writes F16 / BF16 only");
   if (!h) return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: null handle");
   if (M <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: M must be >= 1");
   if (!codes || !s_x || !z_x || !y) return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: null pointer");
@@ -844,6 +848,7 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
   g.ready = ready;
   g.done = ready ? ready + kMaxFlagBlocks : nullptr;
   g.mblocks = static_cast<int>((M + 127) / 128);
+  g.act = act;
   static const bool no_tma_store = [] {
     const char* e = std::getenv("DTQ_DEBUG_NO_TMA_STORE");
     return e && e[0] == '1';
@@ -908,7 +913,7 @@ bool row_flags_wanted(const dtq_qlinear_s* h, int64_t M, int y_dtype) {
 
 int forward_impl(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear_s* h, int mode,
                  const dtq_prologue* pro, void* y, int y_dtype, int64_t ldy, void* ws,
-                 size_t ws_bytes, int32_t* status, cudaStream_t st) {
+                 size_t ws_bytes, int32_t* status, cudaStream_t st, int act = DTQ_ACT_NONE) {
   if (!h) return fail(DTQ_ERR_INVALID_ARGUMENT, "forward: null handle");
   if (ldx < h->K) return fail(DTQ_ERR_INVALID_ARGUMENT, "qlinear_forward: X cols != C_in");
   int64_t ldc;
@@ -928,7 +933,7 @@ int forward_impl(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear
   int32_t* z_x = reinterpret_cast<int32_t*>(base + off_z);
   DTQ_TRY(overflow_check(h->abits, h->wbits, h->K));
   int p_regs = 0, p_smem = 0, flags = 0;
-  if (row_flags_wanted(h, M, y_dtype)) {
+  if (act == DTQ_ACT_NONE && row_flags_wanted(h, M, y_dtype)) {
     DTQ_TRY(check_device());
     const GemmCfg cfg = choose_gemm_cfg(M, h->N, h->wbits, device_info().sms);
     const int kind = y_dtype == DTQ_F16 ? dtq_gemm::kOutF16
@@ -940,7 +945,7 @@ int forward_impl(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear
   DTQ_TRY(quantize_rows_impl(x, x_dtype, M, h->K, ldx, h->abits, 0, mode, 0, h->smooth,
                              h->col_mul, h->signs, h->hblock, pro, codes, ldc, s_x, z_x,
                              status, st, true, ready, p_regs, p_smem, &flags));
-  return qgemm_impl(codes, ldc, s_x, z_x, M, h, y, y_dtype, ldy, st, flags ? ready : nullptr);
+  return qgemm_impl(codes, ldc, s_x, z_x, M, h, y, y_dtype, ldy, st, flags ? ready : nullptr, act);
 }
 
 }  // namespace
@@ -1270,6 +1275,17 @@ int dtq_qlinear_forward(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_
   NvtxRange nvtx_range("dtq_qlinear_forward");
   return forward_impl(x, x_dtype, M, ldx, h, mode, prologue, y, y_dtype, ldy, workspace,
                       workspace_bytes, status, as_stream(stream));
+}
+
+int dtq_qlinear_forward_act(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear_t h,
+                            int mode, const dtq_prologue* prologue, int activation, void* y,
+                            int y_dtype, int64_t ldy, void* workspace, size_t workspace_bytes,
+                            int32_t* status, void* stream) {
+  NvtxRange nvtx_range("dtq_qlinear_forward_act");
+  if (activation != DTQ_ACT_NONE && activation != DTQ_ACT_GELU)
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "forward: bad activation %d", activation);
+  return forward_impl(x, x_dtype, M, ldx, h, mode, prologue, y, y_dtype, ldy, workspace,
+                      workspace_bytes, status, as_stream(stream), activation);
 }
 
 int dtq_qlinear_quantize(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear_t h,

@@ -45,12 +45,12 @@ cudaError_t dtq_launch_gemm_w8_cores(const CUtensorMap& tA, const CUtensorMap& t
                                      const CUtensorMap& tY, const dtq_gemm::GemmArgs& g,
                                      GemmCfg c, int sms, cudaStream_t st);
 
-template <int BN, int kStages, bool kW4, int kOut, bool k2Cta, bool kCoRes = false>
+template <int BN, int kStages, bool kW4, int kOut, bool k2Cta, bool kCoRes = false, int kAct = 0>
 cudaError_t dtq_launch_gemm_t(const CUtensorMap& tA, const CUtensorMap& tB,
                               const CUtensorMap& tY, const dtq_gemm::GemmArgs& g, int sms,
                               cudaStream_t st) {
   using L = dtq_gemm::Smem<BN, kStages, kW4, k2Cta>;
-  auto kern = dtq_gemm::qgemm_kernel<BN, kStages, kW4, kOut, k2Cta, kCoRes>;
+  auto kern = dtq_gemm::qgemm_kernel<BN, kStages, kW4, kOut, k2Cta, kCoRes, kAct>;
   static thread_local int configured_dev = -1;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -96,8 +96,14 @@ cudaError_t dtq_launch_gemm_o(const CUtensorMap& tA, const CUtensorMap& tB,
                               cudaStream_t st) {
   switch (g.out_kind) {
     case dtq_gemm::kOutF16:
+      if (g.act == 1)  // GELU epilogue (fp16 / bf16 outputs)
+        return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutF16, k2Cta, false, 1>(tA, tB, tY,
+                                                                                     g, sms, st);
       return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutF16, k2Cta>(tA, tB, tY, g, sms, st);
     case dtq_gemm::kOutBF16:
+      if (g.act == 1)
+        return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutBF16, k2Cta, false, 1>(tA, tB, tY,
+                                                                                      g, sms, st);
       return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutBF16, k2Cta>(tA, tB, tY, g, sms, st);
     case dtq_gemm::kOutF32:
       return dtq_launch_gemm_t<BN, kStages, kW4, dtq_gemm::kOutF32, k2Cta>(tA, tB, tY, g, sms, st);

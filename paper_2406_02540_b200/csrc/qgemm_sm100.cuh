@@ -27,6 +27,7 @@
 
 #include <cstdint>
 
+#include "gelu.cuh"
 #include "ptx.cuh"
 
 namespace dtq_gemm {
@@ -65,6 +66,7 @@ struct GemmArgs {
   uint32_t* ready;
   uint32_t* done;
   int mblocks;          // ceil(M / 128): counters to reset
+  int act;              // activation on y in the epilogue: 0 none, 1 GELU (fp outputs)
 };
 
 constexpr int BM = 128;
@@ -192,7 +194,9 @@ __device__ __forceinline__ uint2 w4_word_to_s8x8_x16(uint32_t w) {
 // kCoRes: the instance shares every SM with a tile-quantizer CTA (row flags):
 // capped at 112 registers per thread so both CTAs' registers fit the SM (the
 // others at 200, what 320 threads of one CTA per SM allow anyway).
-template <int BN, int kStages, bool kW4, int kOut, bool k2Cta, bool kCoRes = false>
+// kAct: activation applied to the fp32 y before the cast (1 = GELU,
+// toydit.cpp:83 -- the fc1 -> gelu of toydit.cpp:215-216 in fc1's epilogue)
+template <int BN, int kStages, bool kW4, int kOut, bool k2Cta, bool kCoRes = false, int kAct = 0>
 #ifdef DTQ_PLAIN_LB
 __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1)
 #else
@@ -559,8 +563,14 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1) __maxnreg__(kCoRes 
               const float2 yy = __ffma2_rn(
                   make_float2(static_cast<float>(a32[u]), static_cast<float>(a32[u + 1])), sc,
                   make_float2(__uint_as_float(bv[u]), __uint_as_float(bv[u + 1])));
-              f[u] = yy.x;
-              f[u + 1] = yy.y;
+              if constexpr (kAct == 1) {
+                const float2 gy = dtq_act::gelu2(yy);
+                f[u] = gy.x;
+                f[u + 1] = gy.y;
+              } else {
+                f[u] = yy.x;
+                f[u + 1] = yy.y;
+              }
             }
             if constexpr (kOut == kOutF16) {
               const __half2 h0 = __floats2half2_rn(f[0], f[1]);

@@ -5,7 +5,10 @@ static-dynamic channel balance (smooth + 128-block Hadamard) and, where the
 model has one in front of the linear, a fused prologue:
 
   * LN_MODULATE (LayerNorm + adaLN t2i_modulate) before qkv / fc1,
-  * GELU (toydit.cpp:83) before fc2.
+  * GELU (toydit.cpp:83) between fc1 and fc2: by default in fc1's GEMM
+    epilogue (`dtq_qlinear_forward_act`, on fp32 y before the cast), so fc2's
+    quantizer runs with no prologue; `gelu_in_fc1_epilogue=False` puts it in
+    fc2's quantizer prologue instead (round 1).
 
 Data flow per block: every hidden-width linear reads the block input x
 (attention itself is not on the quantized-linear path; its output is stood
@@ -83,9 +86,11 @@ class LinearStack:
     """`blocks` DiT blocks of `layers`, each linear a PlannedLinear."""
 
     def __init__(self, layers, blocks: int, plan: dtq.MixedPrecisionPlan, device, seed: int = 7,
-                 act_bits: int = 8, hblock: int = 128, eps: float = 1e-6):
+                 act_bits: int = 8, hblock: int = 128, eps: float = 1e-6,
+                 gelu_in_fc1_epilogue: bool = True):
         import torch
         self.layers, self.blocks, self.plan, self.dev = layers, blocks, plan, device
+        self.gelu_epi = gelu_in_fc1_epilogue
         g = torch.Generator(device=device).manual_seed(seed)
         signs = {}
         self.linears = []   # per block: {name: PlannedLinear}
@@ -146,7 +151,12 @@ class LinearStack:
                     out = nxt
                 else:
                     out = bufs[(src, n)]
+                act = dtq.ACT_NONE
+                if self.gelu_epi and name.endswith("fc1"):
+                    act = dtq.ACT_GELU  # gelu(fc1(x)) in fc1's epilogue
+                if self.gelu_epi and pro == "gelu":
+                    pro = None          # ... so fc2 quantizes its input as is
                 p = self.mods[b] if pro == "ln_mod" else (self.gelu if pro == "gelu" else None)
-                layer.forward(inp, out=out, prologue=p, workspace=ws)
+                layer.forward(inp, out=out, prologue=p, workspace=ws, activation=act)
             cur = nxt
         return cur

@@ -573,3 +573,36 @@ def test_race_stress_every_tile_config():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr[-2000:]
     assert r.stdout.count('"mismatches": 0') == 5
+
+
+@pytest.mark.parametrize("wb", [8, 4])
+@pytest.mark.parametrize("odt", [torch.float16, torch.bfloat16])
+def test_gelu_epilogue(oracle, wb, odt):
+    # gelu(qlinear_forward(x)) with GELU applied in the GEMM's epilogue on the
+    # fp32 y (the fc1 -> gelu of toydit.cpp:215-216): against the oracle's
+    # exact-erf GELU of the reference epilogue within the output dtype's
+    # tolerance, and against GELU applied to the fp32 output of the plain
+    # forward (the same fp32 y) within one output rounding
+    rng = np.random.default_rng(77 + wb)
+    M, K, N = 1000, 1152, 4608
+    x = activations(rng, M, K)
+    w = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float16)
+    bias = rng.standard_normal(N) * 0.1
+    bal = dtq.Balance(cuda(rng.uniform(0.5, 2.0, K)), cuda(dtq.hadamard_signs(K, 7)), 128)
+    layer = dtq.QuantLinear.create(cuda(w), wb, 8, bias=cuda(bias), balance=bal)
+    xt = cuda(x)
+    y = layer.forward(xt, out_dtype=odt, activation=dtq.ACT_GELU).double().cpu().numpy()
+    y32 = layer.forward(xt, out_dtype=torch.float32).double().cpu().numpy()
+    g32 = oracle.gelu(y32)
+    tol = 2 ** -8 if odt == torch.bfloat16 else 2 ** -11
+    assert np.all(np.abs(y - g32) <= tol * np.abs(g32) + 1e-6), np.abs(y - g32).max()
+    codes, s, z = layer.quantize(xt)
+    rows = np.sort(rng.choice(M, 128, replace=False))
+    wc, sw, _ = layer.export()
+    acc_ref = oracle.qlinear_acc(codes.cpu().numpy()[rows], z.cpu().numpy()[rows], wc,
+                                 np.full(N, 1 << (wb - 1), np.int32))
+    y_ref = oracle.gelu(oracle.qlinear_epilogue(acc_ref, s.cpu().numpy()[rows], sw, bias))
+    err = rel_err(y[rows], y_ref)
+    assert err <= (4e-3 if odt == torch.bfloat16 else REL_TOL), err
+    with pytest.raises(dtq.DtqError):
+        layer.forward(xt, out_dtype=torch.float32, activation=dtq.ACT_GELU)  # F16 / BF16 only

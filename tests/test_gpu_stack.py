@@ -5,7 +5,10 @@ layer checked against the oracle chain on its own device input.
 Per block (toydit.cpp:159-219 order, attention and residuals left out --
 they are not on the quantized-linear path):
     x  --LN+modulate--> qkv (1152 -> 3456)            [checked, not chained]
-    x  --LN+modulate--> fc1 (1152 -> 4608) --fp16--> GELU --> fc2 (4608 -> 1152)
+    x  --LN+modulate--> fc1 (1152 -> 4608) + GELU in fc1's GEMM epilogue
+       --fp16--> fc2 (4608 -> 1152)                    [block 0]
+    x  --LN+modulate--> fc1 --fp16--> GELU prologue of fc2's quantizer --> fc2
+                                                       [block 1: the other placement]
     fc2's fp16 output is the next block's x.
 Every linear carries smooth + 128-block Hadamard balance.  For each layer,
 on sampled token rows (exact: quantization is row-local, quant.cpp:70-73):
@@ -50,9 +53,10 @@ def _layer(rng, K, N, oracle):
     return layer, smooth, signs, bias, wc, sw
 
 
-def _check(oracle, name, layer, x_dev, pre, smooth, signs, bias, wc, sw, rows, prologue, stats):
+def _check(oracle, name, layer, x_dev, pre, smooth, signs, bias, wc, sw, rows, prologue, stats,
+           act=dtq.ACT_NONE):
     codes, s, z = layer.quantize(x_dev, mode=dtq.MODE_FAST, prologue=prologue)
-    y = layer.forward(x_dev, out_dtype=torch.float16, prologue=prologue)
+    y = layer.forward(x_dev, out_dtype=torch.float16, prologue=prologue, activation=act)
     acc = layer.gemm(codes, s, z, out_dtype=torch.int32)
     xr = x_dev[torch.as_tensor(rows, device=DEV)].double().cpu().numpy()
     chain = oracle.rotate_blocks(oracle.scale_x(pre(xr), smooth), signs, 128)
@@ -67,6 +71,8 @@ def _check(oracle, name, layer, x_dev, pre, smooth, signs, bias, wc, sw, rows, p
     acc_ref = oracle.qlinear_acc(c_gpu, z_gpu, wc, np.full(wc.shape[0], 128, np.int32))
     assert np.array_equal(acc.cpu().numpy()[rows].astype(np.int64), acc_ref), name
     y_ref = oracle.qlinear_epilogue(acc_ref, s.cpu().numpy()[rows], sw, bias)
+    if act == dtq.ACT_GELU:  # gelu(y) in the epilogue: against the oracle's exact-erf GELU
+        y_ref = oracle.gelu(y_ref)
     err = np.abs(y.float().cpu().numpy()[rows] - y_ref).max() / np.abs(y_ref).max()
     assert err <= 1e-3, (name, err)
     return y
@@ -90,10 +96,12 @@ def test_c4_two_block_chain(oracle):
         qkv = _layer(rng, D, 3 * D, oracle)
         _check(oracle, f"b{blk}.qkv", qkv[0], x, ln, *qkv[1:], rows, pro_ln, stats)
         fc1 = _layer(rng, D, 4 * D, oracle)
-        h = _check(oracle, f"b{blk}.fc1", fc1[0], x, ln, *fc1[1:], rows, pro_ln, stats)
+        epi = blk == 0  # block 0: GELU in fc1's epilogue; block 1: in fc2's quantizer
+        h = _check(oracle, f"b{blk}.fc1", fc1[0], x, ln, *fc1[1:], rows, pro_ln, stats,
+                   act=dtq.ACT_GELU if epi else dtq.ACT_NONE)
         fc2 = _layer(rng, 4 * D, D, oracle)
-        x = _check(oracle, f"b{blk}.fc2", fc2[0], h, oracle.gelu, *fc2[1:], rows,
-                   dtq.Prologue(dtq.PROLOGUE_GELU), stats)
+        x = _check(oracle, f"b{blk}.fc2", fc2[0], h, (lambda v: v) if epi else oracle.gelu,
+                   *fc2[1:], rows, None if epi else dtq.Prologue(dtq.PROLOGUE_GELU), stats)
         assert bool(torch.isfinite(x).all())
     nd = sum(s[1] for s in stats)
     n = sum(s[2] for s in stats)

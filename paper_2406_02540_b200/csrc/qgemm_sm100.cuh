@@ -294,6 +294,60 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1) __maxnreg__(kCoRes 
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // The stage operations of the producer.  B (the weights, a layer constant)
+  // may be loaded before griddepcontrol.wait; A (the codes) and the
+  // per-token params come from the preceding quantizer kernel.
+  auto arm = [&](int st) {
+    if constexpr (k2Cta && kW4 && L::kP > 0) {
+      // A of both CTAs lands on the leader's barrier; each CTA's packed
+      // nibbles land on its OWN barrier, which its converters wait on
+      mbar_arrive_expect_tx(&full[st], rank == 0 ? 2 * L::kA + L::kP : L::kP);
+    } else if constexpr (k2Cta) {
+      // both CTAs' bytes land on the leader's barrier; only it arms it
+      // (W4A8 on the L2 path: A only, the converters fill B)
+      if (rank == 0) mbar_arrive_expect_tx(&full[st], 2 * (L::kA + (kW4 ? 0 : L::kB)));
+    } else {
+      mbar_arrive_expect_tx(&full[st], L::kA + (kW4 ? L::kP : L::kB));  // kA: both sub-tiles with kM2
+    }
+  };
+  auto load_b = [&](int st, int kb, int n0) {
+    if constexpr (k2Cta && kW4 && L::kP > 0) {
+      tma_load_2d(sP + st * L::kP, &tmB, &full[st], kb * (BK / 2), n0 + rank * L::kBRows);
+    } else if constexpr (k2Cta) {
+      if constexpr (!kW4)
+        tma_load_2d_2sm(sB + st * L::kB, &tmB, mapa_shared(smem_u32(&full[st]), 0), kb * BK,
+                        n0 + rank * L::kBRows);
+    } else {
+      if constexpr (!kW4)
+        tma_load_2d(sB + st * L::kB, &tmB, &full[st], kb * BK, n0);
+      else if constexpr (L::kP > 0)
+        tma_load_2d(sP + st * L::kP, &tmB, &full[st], kb * (BK / 2), n0);
+    }
+  };
+  auto load_a = [&](int st, int kb, int m0) {
+    if constexpr (k2Cta) {
+      tma_load_2d_2sm(sA + st * L::kA, &tmA, mapa_shared(smem_u32(&full[st]), 0), kb * BK, m0);
+    } else {
+      tma_load_2d(sA + st * L::kA, &tmA, &full[st], kb * BK, m0);
+      if constexpr (kM2) tma_load_2d(sA + st * L::kA + BM * BK, &tmA, &full[st], kb * BK, m0 + BM);
+    }
+  };
+  // B of the first stages before the wait: the weights' load latency
+  // overlaps the quantizer's tail instead of following it
+  int npre = 0;
+  if (warp == kTmaWarp && lane == 0) {
+    const int work = ((total_tiles - tile0 + tstride - 1) / tstride) * g.k_blocks;
+    npre = work < kStages ? work : kStages;
+    int tile = tile0, kb = 0;
+    for (int j = 0; j < npre; ++j) {
+      arm(j);
+      load_b(j, kb, tile_n(tile) * BN);
+      if (++kb == g.k_blocks) {
+        kb = 0;
+        tile += tstride;
+      }
+    }
+  }
   // A codes, s_x, z_x come from the preceding quantizer kernel: all of them
   // at once (griddepcontrol.wait), or row block by row block (flags)
   if (!flags) pdl_wait();
@@ -304,6 +358,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1) __maxnreg__(kCoRes 
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
+      int j = 0;  // k-block sequence number (the first npre have their B already)
       for (int tile = tile0; tile < total_tiles; tile += tstride) {
         const int m0 = tile_m(tile) * kTileM + rank * BM;
         const int n0 = tile_n(tile) * BN;
@@ -316,32 +371,13 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1) __maxnreg__(kCoRes 
           }
           fence_proxy_async_global();  // generic-proxy stores -> this thread's TMA reads
         }
-        for (int kb = 0; kb < g.k_blocks; ++kb) {
-          timed_wait(&empty[s], ph ^ 1, pw0);
-          if constexpr (k2Cta && kW4 && L::kP > 0) {
-            // A of both CTAs lands on the leader's barrier; each CTA's packed
-            // nibbles land on its OWN barrier, which its converters wait on
-            const uint32_t lead_full = mapa_shared(smem_u32(&full[s]), 0);
-            mbar_arrive_expect_tx(&full[s], rank == 0 ? 2 * L::kA + L::kP : L::kP);
-            tma_load_2d_2sm(sA + s * L::kA, &tmA, lead_full, kb * BK, m0);
-            tma_load_2d(sP + s * L::kP, &tmB, &full[s], kb * (BK / 2), n0 + rank * L::kBRows);
-          } else if constexpr (k2Cta) {
-            // both CTAs' bytes land on the leader's barrier; only it arms it
-            // (W4A8 on the L2 path: A only, the converters fill B)
-            const uint32_t lead_full = mapa_shared(smem_u32(&full[s]), 0);
-            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (L::kA + (kW4 ? 0 : L::kB)));
-            tma_load_2d_2sm(sA + s * L::kA, &tmA, lead_full, kb * BK, m0);
-            if constexpr (!kW4)
-              tma_load_2d_2sm(sB + s * L::kB, &tmB, lead_full, kb * BK, n0 + rank * L::kBRows);
-          } else {
-            mbar_arrive_expect_tx(&full[s], L::kA + (kW4 ? L::kP : L::kB));
-            tma_load_2d(sA + s * L::kA, &tmA, &full[s], kb * BK, m0);
-            if constexpr (kM2) tma_load_2d(sA + s * L::kA + BM * BK, &tmA, &full[s], kb * BK, m0 + BM);
-            if constexpr (!kW4)
-              tma_load_2d(sB + s * L::kB, &tmB, &full[s], kb * BK, n0);
-            else if constexpr (L::kP > 0)
-              tma_load_2d(sP + s * L::kP, &tmB, &full[s], kb * (BK / 2), n0);
+        for (int kb = 0; kb < g.k_blocks; ++kb, ++j) {
+          if (j >= npre) {
+            timed_wait(&empty[s], ph ^ 1, pw0);
+            arm(s);
+            load_b(s, kb, n0);
           }
+          load_a(s, kb, m0);
           if (++s == kStages) {
             s = 0;
             ph ^= 1;

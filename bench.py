@@ -470,9 +470,10 @@ def run_stack(dev, reps: int = 10):
 # ---------------------------------------------------------------------- W4A8 (C3)
 def run_w4_c3(dev, KB):
     """BASELINE configs[2]: W4A8 at the STDiT block shapes, M=4096: the GEMM
-    alone on pre-quantized codes, and the whole layer (fused quantizer with
-    smooth + 128-block Hadamard, then the GEMM) -- CUDA-graph batches over a
-    >L2 ring of inputs."""
+    alone on pre-quantized codes (the in-GEMM nibble unpack), and the whole
+    layer (fused quantizer with smooth + 128-block Hadamard that also expands
+    the weights to s8 in the workspace, then the W8A8 GEMM) beside the same
+    layer at W8A8 -- CUDA-graph batches over a >L2 ring of inputs."""
     import torch
     import paper_2406_02540_b200 as dtq
     out = {}
@@ -483,6 +484,7 @@ def run_w4_c3(dev, KB):
         signs = torch.from_numpy(dtq.hadamard_signs(k, 7)).to(dev)
         smooth = torch.rand(k, generator=g, device=dev, dtype=torch.float64) + 0.5
         layer = dtq.QuantLinear.create(w, 4, 8, balance=dtq.Balance(smooth, signs, 128))
+        layer8 = dtq.QuantLinear.create(w, 8, 8, balance=dtq.Balance(smooth, signs, 128))
         x = torch.randn(M, k, generator=g, device=dev).half()
         codes, s_x, z_x = layer.quantize(x)
         y = torch.empty(M, n, dtype=torch.float16, device=dev)
@@ -495,18 +497,22 @@ def run_w4_c3(dev, KB):
             for i in range(KB):
                 layer.gemm(ring[i % nb], s_x, z_x, out=y)
 
-        def fwds():
+        def fwds(lay=layer):
             for i in range(KB):
-                layer.forward(xr[i % len(xr)], out=y, workspace=ws)
+                lay.forward(xr[i % len(xr)], out=y, workspace=ws)
 
         t = float(np.median(time_graph(graph_of(gemms), 5))) / KB
         tl = float(np.median(time_graph(graph_of(fwds), 5))) / KB
+        t8 = float(np.median(time_graph(graph_of(lambda: fwds(layer8)), 5))) / KB
         ops = 2.0 * M * n * k
         out[name] = {"M": M, "K": k, "N": n, "gemm_ms": t * 1e3, "gemm_tops": ops / t / 1e12,
-                     "layer_ms": tl * 1e3, "layer_tops": ops / tl / 1e12}
-        del ring, xr
-    out["note"] = ("int4 weights unpacked to s8 in smem; gemm: codes pre-quantized; layer: "
-                   "fused quantizer (smooth + Hadamard) + GEMM per forward; fp16 out")
+                     "layer_ms": tl * 1e3, "layer_tops": ops / tl / 1e12,
+                     "w8a8_layer_ms": t8 * 1e3, "w4_over_w8": t8 / tl}
+        del ring, xr, layer8
+    out["note"] = ("gemm: the standalone W4A8 GEMM on pre-quantized codes, nibbles unpacked "
+                   "to s8 in smem by converter warps; layer: forward = tile quantizer that "
+                   "also expands the weights to s8 in the workspace, then the W8A8 GEMM; "
+                   "w4_over_w8: W4A8 / W8A8 layer throughput; fp16 out")
     return out
 
 

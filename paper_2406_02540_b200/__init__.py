@@ -443,6 +443,12 @@ class PlannedLinear:
     def forward(self, x, t: int, steps: int, **kw):
         return self.select(t, steps).forward(x, **kw)
 
+    def workspace_bytes(self, M: int) -> int:
+        """Forward workspace bytes for up to M rows at any step (the widest
+        of the row's handles: a W4A8 one also holds its unpacked s8 weights)."""
+        return max(lib().dtq_qlinear_workspace_bytes(self.select(r, NUM_RANGES)._h, M)
+                   for r in range(NUM_RANGES))
+
     def close(self):
         if self._h is not None and self._h.value:
             lib().dtq_planned_destroy(self._h)

@@ -228,8 +228,10 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
                        const dtq_prologue* pro, uint8_t* codes, int64_t ldc, double* scale,
                        int32_t* zero, int32_t* status, cudaStream_t st,
                        bool col_mul_const = true, uint32_t* ready = nullptr,
-                       int partner_regs = 0, int partner_smem = 0, int* flags_used = nullptr) {
+                       int partner_regs = 0, int partner_smem = 0, int* flags_used = nullptr,
+                       const dtq_w4::Unpack* w4job = nullptr, int* w4_done = nullptr) {
   if (flags_used) *flags_used = 0;
+  if (w4_done) *w4_done = 0;
   if (rows <= 0 || cols <= 0) return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: empty matrix");
   if (!bits_supported(bits))
     return fail(DTQ_ERR_INVALID_ARGUMENT, "quantize: bits must be one of {2,4,6,8}");
@@ -382,6 +384,8 @@ int quantize_rows_impl(const void* x, int x_dtype, int64_t rows, int64_t cols, i
       a.partner_regs = partner_regs;
       a.partner_smem = partner_smem;
       a.flags_used = flags_used;
+      if (w4job) a.w4 = *w4job;  // the tile kernel also expands a W4A8 forward's weights
+      a.w4_done = w4_done;
       return fq_error(dtq_launch_fq_tile(a, static_cast<int>(es), x_dtype == DTQ_BF16 ? 1 : 0,
                                          signs != nullptr, R, sms, st));
     }
@@ -495,6 +499,18 @@ __global__ void parity_epilogue_kernel(const int32_t* __restrict__ acc, int64_t 
     if (bias) out = __dadd_rn(out, bias[o]);
     y[t * ldy + o] = out;
   }
+}
+
+// W4A8 forward: the s8 weight expansion as its own kernel (w4_unpack.cuh),
+// for quantizer kernels other than the tile kernel.  Launched
+// programmatically after the quantizer: griddepcontrol.wait precedes every
+// store (the previous forward's GEMM reads the same workspace until the
+// quantizer, which waited for it, has completed).
+__global__ void __launch_bounds__(256) w4_unpack_kernel(const dtq_w4::Unpack u) {
+  dtq_ptx::pdl_wait();
+  dtq_ptx::pdl_launch_dependents();
+  dtq_w4::unpack_range(u, blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x,
+                       static_cast<int64_t>(gridDim.x) * blockDim.x);
 }
 
 __global__ void to_f32_kernel(const double* __restrict__ in, float* __restrict__ out, int64_t n,
@@ -772,7 +788,8 @@ unsigned long long* probe_buffer() {
 
 int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32_t* z_x,
                int64_t M, dtq_qlinear_s* h, void* y, int y_dtype, int64_t ldy, cudaStream_t st,
-               uint32_t* ready = nullptr, int act = DTQ_ACT_NONE) {
+               uint32_t* ready = nullptr, int act = DTQ_ACT_NONE,
+               const int8_t* w8_tmp = nullptr) {
   if (act != DTQ_ACT_NONE && act != DTQ_ACT_GELU)
     return fail(DTQ_ERR_INVALID_ARGUMENT, "qgemm: bad activation %d", act);
   if (act != DTQ_ACT_NONE && !(y_dtype == DTQ_F16 || y_dtype == DTQ_BF16))
@@ -785,13 +802,19 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
   DTQ_TRY(overflow_check(h->abits, h->wbits, h->K));
   DTQ_TRY(check_device());
   const int sms = device_info().sms;
-  const GemmCfg cfg = choose_gemm_cfg(M, h->N, h->wbits, sms);
+  // w8_tmp: W4A8 weights unpacked to s8 by this forward (w4_unpack_kernel):
+  // the W8A8 kernels run on them, B read after griddepcontrol.wait
+  const int wbits = w8_tmp ? 8 : h->wbits;
+  const GemmCfg cfg = choose_gemm_cfg(M, h->N, wbits, sms);
   const int BN = cfg.bn;
-  const bool m2 = h->wbits == 4 && !cfg.cta2 && cfg.bn == 128 &&
+  const bool m2 = wbits == 4 && !cfg.cta2 && cfg.bn == 128 &&
                   dtq_gemm::dual_m<128, true, false>();  // two M sub-tiles per CTA
   const int tile_m = (cfg.cta2 || m2) ? 2 * dtq_gemm::BM : dtq_gemm::BM;
   const int brows = cfg.cta2 ? BN / 2 : BN;
-  const CUtensorMap& tB = h->tmB[brows == 256 ? 0 : (brows == 128 ? 1 : 2)];
+  CUtensorMap tB = h->tmB[brows == 256 ? 0 : (brows == 128 ? 1 : 2)];
+  if (w8_tmp)
+    DTQ_TRY(cached_tmap_u8(h, &tB, w8_tmp, h->N, h->K, round_up(h->K, 16), dtq_gemm::BK, brows,
+                           CU_TENSOR_MAP_SWIZZLE_128B));
 
   CUtensorMap tA;
   DTQ_TRY(cached_tmap_u8(h, &tA, codes, M, h->K, ldc, dtq_gemm::BK, dtq_gemm::BM,
@@ -849,6 +872,7 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
   g.done = ready ? ready + kMaxFlagBlocks : nullptr;
   g.mblocks = static_cast<int>((M + 127) / 128);
   g.act = act;
+  g.b_pre = w8_tmp ? 0 : 1;
   static const bool no_tma_store = [] {
     const char* e = std::getenv("DTQ_DEBUG_NO_TMA_STORE");
     return e && e[0] == '1';
@@ -862,7 +886,7 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
                            CU_TENSOR_MAP_SWIZZLE_64B));
 
   const cudaError_t e = ready ? dtq_launch_gemm_w8_cores(tA, tB, tY, g, cfg, sms, st)
-                       : h->wbits != 4 ? dtq_launch_gemm_w8(tA, tB, tY, g, cfg, sms, st)
+                       : wbits != 4 ? dtq_launch_gemm_w8(tA, tB, tY, g, cfg, sms, st)
                                        : dtq_launch_gemm_w4(tA, tB, tY, g, cfg, sms, st);
   if (e != cudaSuccess) return fail(DTQ_ERR_CUDA, "qgemm launch: %s", cudaGetErrorString(e));
 
@@ -877,18 +901,63 @@ int qgemm_impl(const uint8_t* codes, int64_t ldc, const double* s_x, const int32
 }
 
 // workspace: [row-flag counters: kMaxFlagBlocks + the GEMM's exit ticket]
-// [codes M x ldc][s_x f64 M][z_x i32 M].  The counter region has a fixed size
-// (a workspace serves forwards of any M) and must be zero before first use;
-// every forward leaves it zero.
+// [codes M x ldc][s_x f64 M][z_x i32 M] and, for W4A8 handles, [s8 weights
+// N x round_up(K, 16)] (w4_unpack_kernel).  The counter region has a fixed
+// size (a workspace serves forwards of any M) and must be zero before first
+// use; every forward leaves it zero.
 constexpr size_t kFlagBytes = (kMaxFlagBlocks + 64) * sizeof(uint32_t);
 size_t ws_layout(const dtq_qlinear_s* h, int64_t M, int64_t* ldc, size_t* off_codes,
-                 size_t* off_s, size_t* off_z) {
+                 size_t* off_s, size_t* off_z, size_t* off_w = nullptr) {
   *ldc = round_up(h->K, 16);
   *off_codes = kFlagBytes;
   const size_t codes = kFlagBytes + round_up(static_cast<int64_t>(M) * *ldc, 256);
   *off_s = codes;
   *off_z = codes + round_up(M * 8, 256);
-  return *off_z + round_up(M * 4, 256);
+  const size_t end = *off_z + round_up(M * 4, 256);
+  if (off_w) *off_w = h->wbits == 4 ? end : 0;
+  return end + (h->wbits == 4 ? round_up(h->N * round_up(h->K, 16), 256) : 0);
+}
+
+// W4A8 forward through s8 weights unpacked into the workspace (then the
+// W8A8 kernels, CTA pairs included) rather than the GEMM's in-kernel
+// unpack.  DTQ_W4_UNPACK=0 / 1 (diagnostics) forces either.
+bool w4_unpack_wanted(const dtq_qlinear_s* h, int64_t M) {
+  static const int forced = [] {
+    const char* e = std::getenv("DTQ_W4_UNPACK");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (h->wbits != 4) return false;
+  if (forced >= 0) return forced != 0;
+  (void)M;
+  return true;
+}
+
+dtq_w4::Unpack w4_job(const dtq_qlinear_s* h, int8_t* out) {
+  dtq_w4::Unpack u;
+  u.src = h->w4;
+  u.ld4 = h->ld4;
+  u.rows = h->N;
+  u.chunks = (round_up(h->K, 8) / 2 + 15) / 16;
+  u.dst = out;
+  u.ld8 = round_up(h->K, 16);
+  return u;
+}
+
+int launch_w4_unpack(const dtq_w4::Unpack& u, cudaStream_t st) {
+  const int64_t total = u.rows * u.chunks;
+  const int64_t cap = static_cast<int64_t>(device_info().sms) * 8;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, cap)));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, w4_unpack_kernel, u);
+  if (e != cudaSuccess) return fail(DTQ_ERR_CUDA, "w4 unpack launch: %s", cudaGetErrorString(e));
+  return DTQ_OK;
 }
 
 // Row flags for this forward?  The quantizer and the GEMM then run
@@ -917,8 +986,8 @@ int forward_impl(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear
   if (!h) return fail(DTQ_ERR_INVALID_ARGUMENT, "forward: null handle");
   if (ldx < h->K) return fail(DTQ_ERR_INVALID_ARGUMENT, "qlinear_forward: X cols != C_in");
   int64_t ldc;
-  size_t off_c, off_s, off_z;
-  const size_t need = ws_layout(h, M, &ldc, &off_c, &off_s, &off_z);
+  size_t off_c, off_s, off_z, off_w;
+  const size_t need = ws_layout(h, M, &ldc, &off_c, &off_s, &off_z, &off_w);
   if (!ws) {
     DTQ_TRY(grow(&h->scratch, &h->scratch_bytes, need, st, true));
     ws = h->scratch;
@@ -932,6 +1001,11 @@ int forward_impl(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear
   double* s_x = reinterpret_cast<double*>(base + off_s);
   int32_t* z_x = reinterpret_cast<int32_t*>(base + off_z);
   DTQ_TRY(overflow_check(h->abits, h->wbits, h->K));
+  // W4A8: s8 weights expanded into the workspace by the quantizer's CTAs, or
+  // by their own kernel between the quantizer and the GEMM
+  int8_t* w8_tmp = w4_unpack_wanted(h, M) ? reinterpret_cast<int8_t*>(base + off_w) : nullptr;
+  const dtq_w4::Unpack w4u = w8_tmp ? w4_job(h, w8_tmp) : dtq_w4::Unpack{};
+  int w4_done = 0;
   int p_regs = 0, p_smem = 0, flags = 0;
   if (act == DTQ_ACT_NONE && row_flags_wanted(h, M, y_dtype)) {
     DTQ_TRY(check_device());
@@ -944,8 +1018,11 @@ int forward_impl(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear
   }
   DTQ_TRY(quantize_rows_impl(x, x_dtype, M, h->K, ldx, h->abits, 0, mode, 0, h->smooth,
                              h->col_mul, h->signs, h->hblock, pro, codes, ldc, s_x, z_x,
-                             status, st, true, ready, p_regs, p_smem, &flags));
-  return qgemm_impl(codes, ldc, s_x, z_x, M, h, y, y_dtype, ldy, st, flags ? ready : nullptr, act);
+                             status, st, true, ready, p_regs, p_smem, &flags,
+                             w8_tmp ? &w4u : nullptr, &w4_done));
+  if (w8_tmp && !w4_done) DTQ_TRY(launch_w4_unpack(w4u, st));
+  return qgemm_impl(codes, ldc, s_x, z_x, M, h, y, y_dtype, ldy, st, flags ? ready : nullptr, act,
+                    w8_tmp);
 }
 
 }  // namespace

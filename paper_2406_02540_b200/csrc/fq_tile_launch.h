@@ -101,6 +101,7 @@ cudaError_t launch_tile(const dtq_fq::FqArgs& a_in, int R, int nbuf, int sms, cu
     }
   }
   if (a.flags_used) *a.flags_used = a.ready != nullptr ? 1 : 0;
+  if (a.w4_done) *a.w4_done = a.w4.src != nullptr ? 1 : 0;
   const int64_t cap = static_cast<int64_t>(sms) * (occ > 0 ? occ : 1);
   const int grid = static_cast<int>(tiles < cap ? tiles : cap);
   // programmatic dependent launch: the CTAs' setup (barriers, the per-column

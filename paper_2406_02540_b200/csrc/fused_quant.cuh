@@ -37,6 +37,7 @@
 #include <cstdint>
 
 #include "gelu.cuh"
+#include "w4_unpack.cuh"
 
 namespace dtq_fq {
 
@@ -75,6 +76,8 @@ struct FqArgs {
   unsigned long long* probe;  // diagnostics: per-warp phase cycles (or nullptr)
   int tpr;                    // threads per row (multiple of 16 and of hblock/8)
   int dbg;                    // diagnostics (tile kernel): 1 = skip the transform
+  dtq_w4::Unpack w4;          // tile kernel: a W4A8 forward's weight expansion (w4_unpack.cuh)
+  int* w4_done;               // launcher: 1 if the tile kernel took the w4 job
 };
 
 // ------------------------------------------------------------------ GELU

@@ -347,6 +347,11 @@ __global__ void __launch_bounds__(kWide ? 576 : 288, kWide ? 1 : DTQ_FQ_MINB)
     for (int k = 0; k + 1 < nbuf; ++k)
       if (tile + k * static_cast<int64_t>(gridDim.x) < ntiles) issue(tile + k * gridDim.x, k);
   }
+  // a W4A8 forward's s8 weights, expanded while the first tiles arrive (the
+  // GEMM reads them after this grid completes)
+  if (a.w4.src != nullptr)
+    dtq_w4::unpack_range(a.w4, static_cast<int64_t>(blockIdx.x) * blockDim.x + t,
+                         static_cast<int64_t>(gridDim.x) * blockDim.x);
   // folded per-column affine map with the per-call modulate vectors:
   // v -> v * A_c + B_c (or a per-call multiplier alone).  Loads are batched
   // 8 deep per thread.

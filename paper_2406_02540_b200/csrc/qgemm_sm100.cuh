@@ -67,6 +67,9 @@ struct GemmArgs {
   uint32_t* done;
   int mblocks;          // ceil(M / 128): counters to reset
   int act;              // activation on y in the epilogue: 0 none, 1 GELU (fp outputs)
+  int b_pre;            // 1: B is a layer constant (the handle's weights), loaded for the
+                        // first stages before griddepcontrol.wait; 0: B is written by
+                        // an earlier kernel of this forward (W4 weights unpacked to s8)
 };
 
 constexpr int BM = 128;
@@ -337,7 +340,7 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1) __maxnreg__(kCoRes 
   int npre = 0;
   if (warp == kTmaWarp && lane == 0) {
     const int work = ((total_tiles - tile0 + tstride - 1) / tstride) * g.k_blocks;
-    npre = work < kStages ? work : kStages;
+    npre = !g.b_pre ? 0 : work < kStages ? work : kStages;
     int tile = tile0, kb = 0;
     for (int j = 0; j < npre; ++j) {
       arm(j);

@@ -129,9 +129,8 @@ class LinearStack:
                 outs[key] = torch.empty((rows, n), dtype=torch.float16, device=self.dev)
         outs["x"] = [torch.empty((shape.img_rows, HIDDEN), dtype=torch.float16, device=self.dev)
                      for _ in range(2)]
-        ws_bytes = max(dtq.lib().dtq_qlinear_workspace_bytes(self.linears[0][name].select(0, 1)._h,
-                                                             shape.img_rows)
-                       for name, *_ in self.layers)
+        ws_bytes = max(self.linears[b][name].workspace_bytes(shape.img_rows)
+                       for b in range(self.blocks) for name, *_ in self.layers)
         outs["ws"] = torch.zeros(ws_bytes, dtype=torch.uint8, device=self.dev)  # row flags: 0
         return outs
 

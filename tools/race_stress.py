@@ -1,6 +1,7 @@
 """Race detection by repetition (compute-sanitizer is closed on this GPU pool):
 every GEMM tile configuration (1-CTA / CTA pair x BN 256 / 128, W8A8 and
-W4A8 incl. W4 CTA pairs) and the quantizer kernels run the same forwards
+W4A8 incl. W4 CTA pairs, W4A8 forwards on s8 weights expanded into a
+shared workspace) and the quantizer kernels run the same forwards
 hundreds of times back to back, interleaved with other shapes so the
 persistent kernels' pipelines (mbarrier phases, TMEM double buffer, TMA ring,
 converter ring) start in every state; every result must be bit-identical to
@@ -37,6 +38,10 @@ def child(reps):
     sh = torch.randn(1152, device=dev) * 0.1
     pros = {None: None, "gelu": dtq.Prologue(dtq.PROLOGUE_GELU),
             "ln": dtq.Prologue(dtq.PROLOGUE_LN_MODULATE, sc, sh, 1e-6)}
+    # one workspace for every layer, as a network's forward shares it: each
+    # W4A8 forward rewrites the s8 weights the previous layer's GEMM read
+    ws = torch.zeros(max(dtq.lib().dtq_qlinear_workspace_bytes(l._h, x.shape[0])
+                         for (l, _), x in zip(layers, xs)), dtype=torch.uint8, device=dev)
     first = [l.forward(x, prologue=pros[p]).clone() for (l, p), x in zip(layers, xs)]
     acc0 = [l.gemm(*l.quantize(x, prologue=pros[p]), out_dtype=torch.int32).clone()
             for (l, p), x in zip(layers, xs)]
@@ -44,7 +49,7 @@ def child(reps):
     bad = 0
     for r in range(reps):
         for i, ((l, p), x) in enumerate(zip(layers, xs)):
-            y = l.forward(x, prologue=pros[p])
+            y = l.forward(x, prologue=pros[p], workspace=ws)
             if (r & 7) == 0:
                 a = l.gemm(*l.quantize(x, prologue=pros[p]), out_dtype=torch.int32)
                 bad += int(not torch.equal(a, acc0[i]))

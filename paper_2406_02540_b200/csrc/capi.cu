@@ -1389,20 +1389,39 @@ int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_
   DTQ_TRY(grow(&h->hx, &h->hx_bytes, xb));
   DTQ_TRY(grow(&h->hy, &h->hy_bytes, yb));
   CUDA_TRY(cudaMemsetAsync(h->status, 0, sizeof(int32_t), st));
-  // Row chunks (~8 of them, multiples of 128 rows) in a three-stage pipeline:
-  // H2D on one stream, quantize + GEMM of chunk i once its rows have landed,
-  // D2H of chunk i once its GEMM is done, on a third stream (quantization is row-local, so chunks are independent).
-  // The D2H (the larger transfer: N > K columns) then runs back to back from
-  // the first chunk on.  The F64 parity output uses a handle-wide s32
-  // scratch and stays in one piece.
-  static const int nchunks = [] {  // DTQ_HOST_CHUNKS (diagnostics): pipeline depth
+  // Row chunks (multiples of 128 rows) in a three-stage pipeline: H2D on one
+  // stream, quantize + GEMM of chunk i once its rows have landed, D2H of
+  // chunk i once its GEMM is done, on a third stream (quantization is
+  // row-local, so chunks are independent).  The D2H (the larger transfer:
+  // N > K columns) should run back to back from as early as possible, so the
+  // chunks grow geometrically: 128 rows first (its H2D and forward take
+  // ~15 us), then doubling -- each chunk's H2D (K columns in, at the rate
+  // left beside the D2H) lands before the D2H stream reaches it, with one H2D
+  // and one D2H copy per chunk (few copies: every interleaved H2D copy costs
+  // D2H rate).  DTQ_HOST_CHUNKS=n (diagnostics) uses n equal chunks instead.
+  // The F64 parity output uses a handle-wide s32 scratch and stays in one
+  // piece.
+  static const int nchunks = [] {
     const char* e = std::getenv("DTQ_HOST_CHUNKS");
-    return e && std::atoi(e) > 0 ? std::atoi(e) : 8;
+    return e && std::atoi(e) > 0 ? std::atoi(e) : 0;
   }();
-  int64_t chunk = (M + nchunks - 1) / nchunks;
-  chunk = (chunk + 127) / 128 * 128;
-  if (y_dtype == DTQ_F64 || M < 1024) chunk = M;
-  if (chunk >= M) {
+  std::vector<int64_t> rows_of;  // chunk sizes
+  if (!(y_dtype == DTQ_F64 || M < 1024)) {
+    if (nchunks > 0) {
+      const int64_t c = ((M + nchunks - 1) / nchunks + 127) / 128 * 128;
+      for (int64_t r = 0; r < M; r += c) rows_of.push_back(std::min(c, M - r));
+    } else {
+      int64_t c = 128;
+      for (int64_t r = 0; r < M;) {
+        int64_t m = std::min(c, M - r);
+        if (M - r - m < c) m = M - r;  // a short remainder joins the last chunk
+        rows_of.push_back(m);
+        r += m;
+        c *= 2;
+      }
+    }
+  }
+  if (rows_of.size() <= 1) {
     CUDA_TRY(cudaMemcpyAsync(h->hx, x, xb, cudaMemcpyHostToDevice, st));
     DTQ_TRY(forward_impl(h->hx, x_dtype, M, h->K, h, mode, nullptr, h->hy, y_dtype, h->N,
                          nullptr, 0, h->status, st));
@@ -1410,13 +1429,14 @@ int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_
   } else {
     int64_t ldc;
     size_t a_, b_, c_;
-    const size_t wsb = ws_layout(h, chunk, &ldc, &a_, &b_, &c_);
+    const int64_t max_rows = *std::max_element(rows_of.begin(), rows_of.end());
+    const size_t wsb = ws_layout(h, max_rows, &ldc, &a_, &b_, &c_);
     DTQ_TRY(grow(&h->pws, &h->pws_bytes, wsb, st, true));
     for (cudaStream_t& s : h->ps)
       if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     for (cudaEvent_t& e : h->pe)
       if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    const size_t nc = static_cast<size_t>((M + chunk - 1) / chunk);
+    const size_t nc = rows_of.size();
     while (h->ev_in.size() < nc) {
       cudaEvent_t a, b;
       CUDA_TRY(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
@@ -1441,24 +1461,17 @@ int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_
     mark(st);
     CUDA_TRY(cudaEventRecord(h->pe[0], st));  // fork: after the status reset
     for (cudaStream_t s : h->ps) CUDA_TRY(cudaStreamWaitEvent(s, h->pe[0], 0));
-    size_t c = 0;
-    for (int64_t r0 = 0; r0 < M; r0 += chunk, ++c) {
-      const int64_t m = M - r0 < chunk ? M - r0 : chunk;
+    int64_t r0 = 0;
+    for (size_t c = 0; c < nc; r0 += rows_of[c], ++c) {
+      const int64_t m = rows_of[c];
       const size_t xo = xe * static_cast<size_t>(r0) * h->K, yo = ye * static_cast<size_t>(r0) * h->N;
       uint8_t* dx = static_cast<uint8_t*>(h->hx) + xo;
       uint8_t* dy = static_cast<uint8_t*>(h->hy) + yo;
-      // H2D in three pieces: chunk 0, chunk 1, then everything else as one
-      // copy.  Interleaving many small H2D copies with the D2H stream costs
-      // ~12% of the D2H rate on PCIe; the first two small pieces start the
-      // pipeline, the large one lands while chunks 0-1 drain.
-      if (c <= 2) {
-        const int64_t rows = c < 2 ? m : M - r0;
-        CUDA_TRY(cudaMemcpyAsync(dx, static_cast<const uint8_t*>(x) + xo, xe * rows * h->K,
-                                 cudaMemcpyHostToDevice, s_in));
-        CUDA_TRY(cudaEventRecord(h->ev_in[c], s_in));
-        mark(s_in);
-      }
-      CUDA_TRY(cudaStreamWaitEvent(s_cmp, h->ev_in[c < 2 ? c : 2], 0));
+      CUDA_TRY(cudaMemcpyAsync(dx, static_cast<const uint8_t*>(x) + xo, xe * m * h->K,
+                               cudaMemcpyHostToDevice, s_in));
+      CUDA_TRY(cudaEventRecord(h->ev_in[c], s_in));
+      mark(s_in);
+      CUDA_TRY(cudaStreamWaitEvent(s_cmp, h->ev_in[c], 0));
       DTQ_TRY(forward_impl(dx, x_dtype, m, h->K, h, mode, nullptr, dy, y_dtype, h->N, h->pws,
                            h->pws_bytes, h->status, s_cmp));
       CUDA_TRY(cudaEventRecord(h->ev_out[c], s_cmp));

@@ -260,6 +260,21 @@ void dtq_oracle_gelu(double* x, int64_t n) {
   for (int64_t i = 0; i < n; ++i) x[i] = 0.5 * x[i] * (1.0 + erf(x[i] / sqrt2));
 }
 
+void dtq_oracle_layernorm(double* x, int64_t rows, int64_t cols, double eps) {
+  /* no reference counterpart; torch.nn.functional.layer_norm semantics:
+   * mean, biased variance of the centred values, (x - mean) / sqrt(var + eps) */
+  for (int64_t r = 0; r < rows; ++r) {
+    double* v = x + r * cols;
+    double mean = 0.0, var = 0.0;
+    for (int64_t c = 0; c < cols; ++c) mean += v[c];
+    mean /= (double)cols;
+    for (int64_t c = 0; c < cols; ++c) var += (v[c] - mean) * (v[c] - mean);
+    var /= (double)cols;
+    const double inv = 1.0 / sqrt(var + eps);
+    for (int64_t c = 0; c < cols; ++c) v[c] = (v[c] - mean) * inv;
+  }
+}
+
 int dtq_oracle_overflow_guard(int act_bits, int weight_bits, int64_t c_in) {
   /* qgemm.cpp:29-34 */
   const int64_t max_term = (int64_t)((1 << act_bits) - 1) * ((int64_t)1 << (weight_bits - 1));

@@ -74,6 +74,11 @@ void dtq_oracle_modulate(double* x, int64_t rows, int64_t cols, const double* sc
 
 /* toydit.cpp:83: 0.5 x (1 + erf(x / sqrt 2)) */
 void dtq_oracle_gelu(double* x, int64_t n);
+/* LayerNorm over each row, no affine (the LN of the north_star's LN-modulate
+ * prologue).  The reference has no LayerNorm: semantics of
+ * torch.nn.functional.layer_norm (biased variance, eps inside the sqrt),
+ * pinned against it in fp64 by tests/test_oracle.py. */
+void dtq_oracle_layernorm(double* x, int64_t rows, int64_t cols, double eps);
 
 /* qgemm.cpp:29-34 int64 overflow guard: returns 2 if it would throw. */
 int dtq_oracle_overflow_guard(int act_bits, int weight_bits, int64_t c_in);

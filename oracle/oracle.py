@@ -73,6 +73,7 @@ class Oracle:
         L.dtq_oracle_scale_w.argtypes = [_p, _i64, _i64, _p]
         L.dtq_oracle_modulate.argtypes = [_p, _i64, _i64, _p, _p]
         L.dtq_oracle_gelu.argtypes = [_p, _i64]
+        L.dtq_oracle_layernorm.argtypes = [_p, _i64, _i64, _dbl]
         L.dtq_oracle_overflow_guard.argtypes = [_int, _int, _i64]
         L.dtq_oracle_qlinear_acc.argtypes = [_p, _p, _i64, _i64, _p, _p, _i64, _p, _int]
         L.dtq_oracle_qlinear_epilogue.argtypes = [_p, _p, _i64, _p, _p, _i64, _p]
@@ -173,6 +174,13 @@ class Oracle:
     def gelu(self, x):
         x = _f64(x).copy()
         self.lib.dtq_oracle_gelu(_ptr(x), x.size)
+        return x
+
+    def layernorm(self, x, eps: float = 1e-6):
+        """Row LayerNorm, no affine (no reference counterpart; pinned against
+        torch.nn.functional.layer_norm in fp64)."""
+        x = _f64(x).copy()
+        self.lib.dtq_oracle_layernorm(_ptr(x), x.shape[0], x.shape[1], float(eps))
         return x
 
     # qgemm.cpp -----------------------------------------------------------

@@ -260,8 +260,8 @@ def test_prologue_modulate_exact(oracle):
 @pytest.mark.parametrize("K", [1152, 1408, 3456, 4608])  # odd block counts: idle items
 def test_prologue_gelu_and_layernorm_codes(oracle, K):
     # GELU follows toydit.cpp:83 (the oracle's exact-erf gelu); LayerNorm has
-    # no reference oracle (parity unpinned), so its chain is an fp64
-    # restatement (biased variance, eps inside the sqrt).  Fast-mode codes
+    # no reference counterpart, so its chain is the oracle's fp64 LayerNorm,
+    # pinned against torch's F.layer_norm (tests/test_oracle.py).  Fast-mode codes
     # against the fp64 chain: within 1 LSB on at most 1e-4 of codes, the
     # north_star bar for fp32 transforms.
     rng = np.random.default_rng(9)
@@ -277,8 +277,7 @@ def test_prologue_gelu_and_layernorm_codes(oracle, K):
     sh = (rng.standard_normal(K) * 0.1).astype(np.float32)
     pro = dtq.Prologue(dtq.PROLOGUE_LN_MODULATE, cuda(sc), cuda(sh), 1e-6)
     codes, s, z = dtq.quantize_rows(xt, prologue=pro)
-    mu = xd.mean(1, keepdims=True)
-    ln = (xd - mu) / np.sqrt(((xd - mu) ** 2).mean(1, keepdims=True) + 1e-6)
+    ln = oracle.layernorm(xd, 1e-6)
     c_ref, s_ref, z_ref = oracle.quantize_rows(oracle.modulate(ln, f64(sc), f64(sh)), 8)
     d = np.abs(codes.cpu().numpy().astype(int) - c_ref.astype(int))
     print(f"LN-modulate K={K}: {(d > 0).mean():.2e} of codes differ")

@@ -17,8 +17,8 @@ on sampled token rows (exact: quantization is row-local, quant.cpp:70-73):
   * the int32 accumulator the oracle computes from the GPU's own codes
     equals the device's (qgemm.cpp:52-60);
   * fp16 y within 1e-3 of max|y_ref| (test_qgemm.cpp:19-26).
-The oracle chain: oracle.modulate / fp64 LayerNorm restatement (no
-reference LN, parity unpinned) / oracle.gelu (toydit.cpp:83), then
+The oracle chain: oracle.modulate / oracle.layernorm (no reference LN;
+pinned against torch's F.layer_norm in fp64) / oracle.gelu (toydit.cpp:83), then
 scale_x + rotate_blocks + quantize_rows, qlinear_acc, qlinear_epilogue.
 """
 import numpy as np
@@ -36,9 +36,7 @@ EPS = 1e-6
 
 
 def _ln_mod(oracle, xd, sc, sh):
-    mu = xd.mean(1, keepdims=True)
-    var = ((xd - mu) ** 2).mean(1, keepdims=True)
-    return oracle.modulate((xd - mu) / np.sqrt(var + EPS), sc, sh)
+    return oracle.modulate(oracle.layernorm(xd, EPS), sc, sh)
 
 
 def _layer(rng, K, N, oracle):

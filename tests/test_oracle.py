@@ -175,3 +175,22 @@ def test_overflow_guard(oracle):
     # qgemm.cpp:29-34: int64 bound is never hit at realistic sizes
     assert oracle.overflow_guard(8, 8, 1 << 40) == 0
     assert oracle.overflow_guard(8, 8, 1 << 50) == 2
+
+
+def test_layernorm_pinned_to_torch(oracle):
+    # the reference has no LayerNorm: the oracle's restatement (used as the
+    # checker of the LN-modulate prologue) is pinned against PyTorch's
+    # F.layer_norm in fp64 -- biased variance, eps inside the sqrt
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(17)
+    x = rng.standard_normal((64, 1152)) * np.exp(rng.standard_normal(1152)) + 3.0
+    x[0] = 7.25                      # constant row: 0 / sqrt(eps)
+    x[1, :] = rng.standard_normal(1152) * 1e-4 + 1e4  # large offset, tiny spread
+    for eps in (1e-6, 1e-5):
+        got = oracle.layernorm(x, eps)
+        want = torch.nn.functional.layer_norm(torch.from_numpy(x), (1152,), eps=eps).numpy()
+        d = np.abs(got - want).max(axis=1)
+        # row 1 is ill-conditioned (offset / spread = 1e8): both sums cancel
+        # ~1e4 * 2^-52 / 1e-4 ~ 2e-8 of a unit value; every other row agrees
+        # to rounding
+        assert d[1] <= 1e-7 and np.delete(d, 1).max() <= 1e-12, d.max()

@@ -29,9 +29,7 @@ def chain(xd, pro, sc, sh, smooth, signs, eps=1e-6):
     elif pro == "mod":
         xd = orc.modulate(xd, sc, sh)
     elif pro == "ln":
-        mu = xd.mean(1, keepdims=True)
-        var = ((xd - mu) ** 2).mean(1, keepdims=True)
-        xd = orc.modulate((xd - mu) / np.sqrt(var + eps), sc, sh)
+        xd = orc.modulate(orc.layernorm(xd, eps), sc, sh)
     if smooth is not None:
         xd = orc.scale_x(xd, smooth)
     if signs is not None:

@@ -563,8 +563,29 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1) __maxnreg__(kCoRes 
               mbar_arrive(&tempty[acc]);
           }
         }
-        if (kOut == kOutNone || GEMM_DBG(g) == 2) {
+        // diagnostics 14: the warps sharing the MMA warp's SMSP drain TMEM
+        // only (their rows get no output); 13: they nap after each chunk
+        if (GEMM_DBG(g) == 13 && (warp & 3) == (kMmaWarp & 3)) __nanosleep(300);
+        if (kOut == kOutNone || GEMM_DBG(g) == 2 || (GEMM_DBG(g) >= 10 && GEMM_DBG(g) <= 12) ||
+            (GEMM_DBG(g) == 14 && (warp & 3) == (kMmaWarp & 3))) {
           if (kLdSets == 2 && cl + 1 < kCols / 32) tmem_ld_wait_regs(rr[(cl + 1) % kLdSets]);
+          // diagnostics 10-12: FFMA2 busy work the size of the dequant math
+          // (~3.5 instructions per value) on all epilogue warps (10), only on
+          // those sharing the MMA warp's SMSP (11), or only on the others (12)
+          const int dg = GEMM_DBG(g);
+          const bool same = (warp & 3) == (kMmaWarp & 3);
+          if (dg == 10 || (dg == 11 && same) || (dg == 12 && !same)) {
+            float2 a4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              a4[u] = make_float2(__uint_as_float(r[2 * u]), __uint_as_float(r[2 * u + 1]));
+            const float2 m = make_float2(1.0001f, 0.9999f), c = make_float2(0.5f, -0.5f);
+#pragma unroll 4
+            for (int i = 0; i < 28; ++i)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) a4[u] = __ffma2_rn(a4[u], m, c);
+            if (a4[0].x + a4[1].y + a4[2].x + a4[3].y == 1.2345f) static_cast<uint32_t*>(g.y)[0] = 1u;
+          }
           continue;
         }
 #pragma unroll
@@ -600,7 +621,10 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1) __maxnreg__(kCoRes 
                                            make_float2(__uint_as_float(swv[u]),
                                                        __uint_as_float(swv[u + 1])));
               const float2 yy = __ffma2_rn(
-                  make_float2(static_cast<float>(a32[u]), static_cast<float>(a32[u + 1])), sc,
+                  GEMM_DBG(g) == 15  // diagnostics: no I2FP (bits reinterpreted)
+                      ? make_float2(__int_as_float(a32[u]), __int_as_float(a32[u + 1]))
+                      : make_float2(static_cast<float>(a32[u]), static_cast<float>(a32[u + 1])),
+                  sc,
                   make_float2(__uint_as_float(bv[u]), __uint_as_float(bv[u + 1])));
               if constexpr (kAct == 1) {
                 const float2 gy = dtq_act::gelu2(yy);

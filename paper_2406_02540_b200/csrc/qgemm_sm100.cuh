@@ -698,7 +698,11 @@ __global__ void __launch_bounds__(num_threads<BN, kW4>(), 1) __maxnreg__(kCoRes 
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmY, sb, col0 * esize, m0 + qrow);
+              if (GEMM_DBG(g) == 16)  // diagnostics: each CTA re-stores onto one tile of its own
+                tma_store_2d(&tmY, sb, (col0 - n0) * esize,
+                             static_cast<int>((blockIdx.x * BM) % static_cast<unsigned>(g.M)) + qrow);
+              else
+                tma_store_2d(&tmY, sb, col0 * esize, m0 + qrow);
               bulk_commit();
             }
             buf = (buf + 1) % kBufs;

@@ -100,3 +100,16 @@ def test_workspace_size_covers_unpacked_weights():
     x = torch.randn(100, 1152, device=DEV).half()
     with pytest.raises(ValueError):
         w4.forward(x, workspace=small)
+
+
+def test_forward_host_pipeline_w4():
+    # the host pipeline's geometric row chunks (128, 256, 512, 1024, rest)
+    # share one workspace: every chunk's quantizer re-expands the weights
+    rng = np.random.default_rng(8)
+    layer, _ = _layer(rng, 4608, 1152)
+    x = torch.from_numpy(rng.standard_normal((4096, 1152)).astype(np.float16))
+    want = layer.forward(x.to(DEV)).cpu()
+    xh = x.pin_memory()
+    yh = torch.empty((4096, 4608), dtype=torch.float16).pin_memory()
+    layer.forward_host(xh, yh)
+    assert torch.equal(yh, want)

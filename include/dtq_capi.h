@@ -169,7 +169,8 @@ int dtq_qgemm(const uint8_t* codes, int64_t ldc, const double* s_x, const int32_
  * `workspace` [dev] of dtq_qlinear_workspace_bytes(h, M) bytes (row-flag
  * counters, codes and per-token params; for a W4A8 handle also its weights
  * expanded to s8, N x round_up(K, 16) bytes, which the quantizer writes and
- * the W8A8 GEMM reads), or NULL to use a handle-owned buffer.  A caller workspace must be zero-filled before its first use (its
+ * the W8A8 GEMM reads; 16-byte aligned), or NULL to use a handle-owned
+ * buffer.  A caller workspace must be zero-filled before its first use (its
  * first 33 KB are the counters through which the GEMM consumes row blocks as
  * the concurrently running quantizer publishes them); every forward leaves
  * them zero again.  Calls that use

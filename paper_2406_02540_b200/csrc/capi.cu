@@ -994,6 +994,9 @@ int forward_impl(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq_qlinear
   } else if (ws_bytes < need) {
     return fail(DTQ_ERR_INVALID_ARGUMENT, "forward: workspace too small (%zu < %zu)", ws_bytes,
                 need);
+  } else if (reinterpret_cast<uintptr_t>(ws) % 16 != 0) {
+    // the codes and the W4A8 s8 weights are TMA operands
+    return fail(DTQ_ERR_INVALID_ARGUMENT, "forward: workspace must be 16-byte aligned");
   }
   uint8_t* base = static_cast<uint8_t*>(ws);
   uint32_t* ready = reinterpret_cast<uint32_t*>(base);

@@ -113,3 +113,15 @@ def test_forward_host_pipeline_w4():
     yh = torch.empty((4096, 4608), dtype=torch.float16).pin_memory()
     layer.forward_host(xh, yh)
     assert torch.equal(yh, want)
+
+
+def test_unaligned_workspace_is_rejected():
+    # the workspace holds TMA operands (codes; a W4A8 forward's s8 weights)
+    rng = np.random.default_rng(12)
+    layer, _ = _layer(rng, 1152, 1152)
+    x = torch.from_numpy(rng.standard_normal((700, 1152)).astype(np.float16)).to(DEV)
+    n = dtq.lib().dtq_qlinear_workspace_bytes(layer._h, 700)
+    big = torch.zeros(n + 64, dtype=torch.uint8, device=DEV)
+    with pytest.raises(ValueError, match="16-byte aligned"):
+        layer.forward(x, workspace=big[8:8 + n])
+    assert torch.equal(layer.forward(x, workspace=big[16:16 + n]), layer.forward(x))

@@ -206,7 +206,10 @@ int dtq_qlinear_quantize(const void* x, int x_dtype, int64_t M, int64_t ldx, dtq
 
 /* Same with HOST buffers (x [host] M x K dense, y [host] M x N dense):
  * H2D copy, fused forward, D2H copy, stream synchronised before returning.
- * Pinned host memory gives full PCIe/C2C bandwidth.  Non-finite input is
+ * From 1024 rows (non-F64 outputs) the rows run as a pipeline of chunks of
+ * 128, 256, 512, ... rows on three internal streams (H2D / forward / D2H), so
+ * the D2H of early chunks overlaps the rest.  Pinned host memory gives full
+ * PCIe/C2C bandwidth.  Non-finite input is
  * reported as DTQ_ERR_INVALID_ARGUMENT (the reference's exception).
  * Thread-safe: concurrent calls on one handle are serialised (the handle
  * owns the staging buffers and streams). */

@@ -1414,13 +1414,22 @@ int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_
       const int64_t c = ((M + nchunks - 1) / nchunks + 127) / 128 * 128;
       for (int64_t r = 0; r < M; r += c) rows_of.push_back(std::min(c, M - r));
     } else {
-      int64_t c = 128;
+      // DTQ_HOST_FIRST / DTQ_HOST_GROWTH (diagnostics): first chunk, growth
+      static const int64_t first = [] {
+        const char* e = std::getenv("DTQ_HOST_FIRST");
+        return e && std::atoll(e) >= 128 ? std::atoll(e) / 128 * 128 : 128;
+      }();
+      static const int64_t growth = [] {
+        const char* e = std::getenv("DTQ_HOST_GROWTH");
+        return e && std::atoll(e) >= 2 ? std::atoll(e) : 2;
+      }();
+      int64_t c = first;
       for (int64_t r = 0; r < M;) {
         int64_t m = std::min(c, M - r);
         if (M - r - m < c) m = M - r;  // a short remainder joins the last chunk
         rows_of.push_back(m);
         r += m;
-        c *= 2;
+        c *= growth;
       }
     }
   }

@@ -1,6 +1,20 @@
-import os, sys, torch
-sys.path.insert(0, "/root/repo")
-import paper_2406_02540_b200 as dtq
+"""GEMM time with random vs all-zero operands, per diagnostics mode
+(profiles/r02_gemm_epilogue_smsp.md).
+
+usage: [DTQ_B200_LIB=variants/diag/libdtq_b200.so DTQ_DEBUG_GEMM_EPI=n] [TAG=name]
+       python tools/power_probe.py
+W8A8 GEMM at C2 (4096 x 4608 x 1152) and 16384 rows, fp16 out, CUDA graph of
+20 launches over a >L2 ring of code buffers; "zero" = all-zero activation
+codes and zero weights (minimal operand toggling).  Diagnostics.
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2406_02540_b200 as dtq  # noqa: E402
+
 dev = torch.device("cuda:0")
 def run(M, N, K, zero):
     if zero:

@@ -219,7 +219,7 @@ int dtq_qlinear_forward_host(const void* x, int x_dtype, int64_t M, dtq_qlinear_
 /* ---------------------------------------------------------------- fp64 parity kernels
  * Device implementations of the remaining reference operations, in fp64 and
  * in the reference's operation order (bit-identical results).  Used by the
- * C++ drop-in (include/dtq/*.hpp); not on the timed path.
+ * C++ drop-in (the include/dtq/ headers); not on the timed path.
  *
  * grouping: 0 PerTensor, 1 PerToken, 2 PerChannel, 3 PerOutputChannel,
  *           4 PerGroup(group_size)   (quant.hpp:26-48 GroupingScheme::kind)

@@ -88,3 +88,33 @@ def test_planned_layer_rejects_unquantized_widths_before_the_device():
     bits = (ctypes.c_int32 * 4)(8, 16, 4, 4)  # 16 = the reference's FP passthrough
     st = L.dtq_planned_create(1, dtq.F16, 4, 8, 8, bits, 8, None, None, None, ctypes.byref(h))
     assert st == dtq.DTQ_ERR_INVALID_ARGUMENT and b"range 1" in L.dtq_last_error()
+
+
+def _build_c_example(tmp_path):
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None or not os.path.exists(dtq.LIB_PATH):
+        pytest.skip("no C compiler or libdtq_b200.so not built")
+    libdir = os.path.dirname(dtq.LIB_PATH)
+    exe = str(tmp_path / "capi_example")
+    r = subprocess.run([cc, "-std=c11", "-Wall", "-Wextra", "-Werror", "-O2",
+                        "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include",
+                        os.path.join(ROOT, "tests", "capi_example.c"), "-o", exe,
+                        "-L" + libdir, "-ldtq_b200", "-L/usr/local/cuda/lib64", "-lcudart", "-lm",
+                        "-Wl,-rpath," + libdir], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_caller_compiles_and_refuses_without_device(tmp_path):
+    # include/dtq_capi.h is plain C11 (what cgo / JNI / N-API bind); without
+    # a sm_100 device every compute entry point returns DTQ_ERR_CUDA
+    import subprocess
+    import torch
+    exe = _build_c_example(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    if torch.cuda.is_available():
+        assert r.returncode == 0 and "ok:" in r.stdout, r.stdout + r.stderr
+    else:
+        assert r.returncode == 3, r.stdout + r.stderr
